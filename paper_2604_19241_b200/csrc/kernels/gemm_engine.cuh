@@ -1,0 +1,199 @@
+// The warp-specialised role loop of the grouped-GEMM engine (see gemm_core.cuh).
+// Mode supplies operand majors, the per-tile TMA coordinates and the epilogue.
+#pragma once
+#include "gemm_core.cuh"
+
+namespace eplab_dev {
+
+// Tensor maps travel as __grid_constant__ kernel parameters.
+struct TmaPair {
+  CUtensorMap a;
+  CUtensorMap b;
+};
+
+// Called once per CTA after barriers/TMEM are set up. `first` is the first
+// tile task (already claimed by the CTA while it was resolving pre-tasks).
+// Returns the first task id claimed that lies beyond the tile range
+// (so the caller can continue with post-tasks), or TASK_STOP.
+template <class Mode>
+__device__ int gemm_roles(const typename Mode::Args& args, const TmaPair& tm, uint8_t* tiles_smem,
+                          GemmSmem* S, int first, int tile_lo, int tile_hi,
+                          int* __restrict__ cursor) {
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = lane_id();
+  uint8_t* sA = tiles_smem;
+  uint8_t* sB = tiles_smem + STAGES * A_STAGE_BYTES;
+  int beyond = TASK_STOP;
+
+  if (warp == 3) {
+    // ---------------- scheduler: forwards tile ids, stops at the first non-tile id
+    if (lane == 0) {
+      int id = first;
+      for (int it = 0;; ++it) {
+        const int slot = it % RING;
+        mbar_wait(&S->rempty[slot], ((it / RING) & 1) ^ 1);
+        const bool is_tile = id >= tile_lo && id < tile_hi;
+        S->ring[slot] = is_tile ? id - tile_lo : TASK_STOP;
+        mbar_arrive(&S->rfull[slot]);
+        if (!is_tile) {
+          beyond = id;
+          break;
+        }
+        id = atomicAdd(cursor, 1);
+      }
+      S->bcast = beyond;
+    }
+  } else if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      tma_prefetch_desc(&tm.a);
+      tma_prefetch_desc(&tm.b);
+      uint32_t stage = 0, phase = 0;
+      for (int it = 0;; ++it) {
+        const int slot = it % RING;
+        mbar_wait(&S->rfull[slot], (it / RING) & 1);
+        const int t = S->ring[slot];
+        mbar_arrive(&S->rempty[slot]);
+        if (t == TASK_STOP) break;
+        const TileDesc td = Mode::tile(args, t);
+        Mode::before_loads(args, td);
+        for (int kb = 0; kb < td.nkb; ++kb) {
+          mbar_wait(&S->empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&S->full[stage], A_STAGE_BYTES + B_STAGE_BYTES);
+          uint8_t* a = sA + stage * A_STAGE_BYTES;
+          uint8_t* b = sB + stage * B_STAGE_BYTES;
+          Mode::load_a(args, tm, &S->full[stage], a, td, kb);
+          Mode::load_b(args, tm, &S->full[stage], b, td, kb);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- UMMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(BM, BN, Mode::A_MN, Mode::B_MN);
+      const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+      uint32_t stage = 0, phase = 0;
+      for (int it = 0;; ++it) {
+        const int slot = it % RING;
+        mbar_wait(&S->rfull[slot], (it / RING) & 1);
+        const int t = S->ring[slot];
+        mbar_arrive(&S->rempty[slot]);
+        if (t == TASK_STOP) break;
+        const TileDesc td = Mode::tile(args, t);
+        const uint32_t acc = it & 1;
+        mbar_wait(&S->tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = S->tmem_base + acc * BN;
+        for (int kb = 0; kb < td.nkb; ++kb) {
+          mbar_wait(&S->full[stage], phase);
+          tc_fence_after();
+          const uint32_t as = a0 + stage * A_STAGE_BYTES;
+          const uint32_t bs = b0 + stage * B_STAGE_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = Mode::A_MN ? make_sdesc(as + k * 2048, 8192, 1024)
+                                           : make_sdesc(as + k * 32, 16, 1024);
+            const uint64_t bd = Mode::B_MN ? make_sdesc(bs + k * 2048, 8192, 1024)
+                                           : make_sdesc(bs + k * 32, 16, 1024);
+            umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit(&S->empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&S->tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: warp q owns TMEM lanes / tile rows [32q, 32q+32)
+    const int q = warp & 3;
+    const int r = q * 32 + (int)lane;
+    for (int it = 0;; ++it) {
+      const int slot = it % RING;
+      mbar_wait(&S->rfull[slot], (it / RING) & 1);
+      const int t = S->ring[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S->rempty[slot]);
+      if (t == TASK_STOP) break;
+      const TileDesc td = Mode::tile(args, t);
+      const uint32_t acc = it & 1;
+      mbar_wait(&S->tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = S->tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
+      Mode::epilogue(args, td, taddr, r);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S->tempty[acc]);
+    }
+  }
+  __syncthreads();
+  return S->bcast;
+}
+
+// Barrier + TMEM setup shared by every kernel built on the engine.
+__device__ __forceinline__ void gemm_setup(GemmSmem* S) {
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&S->full[i], 1);
+      mbar_init(&S->empty[i], 1);
+    }
+    for (int i = 0; i < ACC_STAGES; ++i) {
+      mbar_init(&S->tfull[i], 1);
+      mbar_init(&S->tempty[i], 4);
+    }
+    for (int i = 0; i < RING; ++i) {
+      mbar_init(&S->rfull[i], 1);
+      mbar_init(&S->rempty[i], 6);  // producer + mma + 4 epilogue warps
+    }
+    S->bcast = TASK_STOP;
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(&S->tmem_base, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+}
+
+__device__ __forceinline__ void gemm_teardown(GemmSmem* S) {
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if ((threadIdx.x >> 5) == 2) tmem_dealloc(S->tmem_base, TMEM_COLS);
+}
+
+// Row-chunk helpers used by epilogues: 32 fp32 accumulators of one row.
+__device__ __forceinline__ void acc_chunk(uint32_t taddr, int chunk, float (&v)[32]) {
+  uint32_t r[32];
+  tmem_ld32(taddr + chunk * 32, r);
+  tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void store_row_bf16_32(__nv_bfloat16* dst, const float (&v)[32]) {
+  int4* d = reinterpret_cast<int4*>(dst);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int4 w;
+    w.x = (int)pack_bf16(v[8 * i + 0], v[8 * i + 1]);
+    w.y = (int)pack_bf16(v[8 * i + 2], v[8 * i + 3]);
+    w.z = (int)pack_bf16(v[8 * i + 4], v[8 * i + 5]);
+    w.w = (int)pack_bf16(v[8 * i + 6], v[8 * i + 7]);
+    d[i] = w;
+  }
+}
+
+__device__ __forceinline__ void store_zero_32(__nv_bfloat16* dst) {
+  int4* d = reinterpret_cast<int4*>(dst);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) d[i] = make_int4(0, 0, 0, 0);
+}
+
+}  // namespace eplab_dev

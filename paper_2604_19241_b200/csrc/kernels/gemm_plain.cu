@@ -1,0 +1,205 @@
+// Plain grouped GEMMs on the tcgen05 engine (no fused collective):
+//   eplab_grouped_gemm_nt : C[m, n] = sum_k A[m, k] * B[e][n, k]   (both K-major; forward shape)
+//   eplab_grouped_gemm_tn : C[e][i, j] = sum_m A[m, i] * B[m, j]   (both MN-major; the transposed
+//                           GroupGEMM of the weight gradient)
+// These are the building blocks of the unfused baseline and the engine's
+// own numerics tests; the MegaKernels reuse the same engine with fused roles.
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "gemm_engine.cuh"
+#include "tma_host.hpp"
+#include "eplab_b200.h"
+
+namespace eplab_dev {
+
+struct ModeNT {
+  static constexpr int A_MN = 0, B_MN = 0;
+  struct Args {
+    const TileDesc* tiles;
+    __nv_bfloat16* C;
+    int ldc;
+    int n_per_expert;  // rows of B per expert
+  };
+  __device__ static TileDesc tile(const Args& a, int t) { return a.tiles[t]; }
+  __device__ static void before_loads(const Args&, const TileDesc&) {}
+  __device__ static void load_a(const Args&, const TmaPair& tm, uint64_t* bar, uint8_t* s,
+                                const TileDesc& td, int kb) {
+    tma_load_2d(&tm.a, bar, s, kb * BK, td.m0);
+  }
+  __device__ static void load_b(const Args& a, const TmaPair& tm, uint64_t* bar, uint8_t* s,
+                                const TileDesc& td, int kb) {
+    tma_load_2d(&tm.b, bar, s, kb * BK, td.e * a.n_per_expert + td.n0);
+  }
+  __device__ static void epilogue(const Args& a, const TileDesc& td, uint32_t taddr, int r) {
+    __nv_bfloat16* row = a.C + (size_t)(td.m0 + r) * a.ldc + td.n0;
+    const bool live = r < td.rows;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      float v[32];
+      acc_chunk(taddr, c, v);
+      if (live) store_row_bf16_32(row + c * 32, v);
+    }
+  }
+};
+
+struct ModeTN {
+  static constexpr int A_MN = 1, B_MN = 1;
+  struct Args {
+    const TileDesc* tiles;
+    __nv_bfloat16* C;  // [E][rows_out][ldc]
+    int ldc;
+    long long expert_stride;
+  };
+  __device__ static TileDesc tile(const Args& a, int t) { return a.tiles[t]; }
+  __device__ static void before_loads(const Args&, const TileDesc&) {}
+  __device__ static void load_a(const Args&, const TmaPair& tm, uint64_t* bar, uint8_t* s,
+                                const TileDesc& td, int kb) {
+#pragma unroll
+    for (int i = 0; i < BM / 64; ++i)
+      tma_load_2d(&tm.a, bar, s + i * 8192, td.m0 + 64 * i, td.kb0 + kb * BK);
+  }
+  __device__ static void load_b(const Args&, const TmaPair& tm, uint64_t* bar, uint8_t* s,
+                                const TileDesc& td, int kb) {
+#pragma unroll
+    for (int i = 0; i < BN / 64; ++i)
+      tma_load_2d(&tm.b, bar, s + i * 8192, td.n0 + 64 * i, td.kb0 + kb * BK);
+  }
+  __device__ static void epilogue(const Args& a, const TileDesc& td, uint32_t taddr, int r) {
+    __nv_bfloat16* row = a.C + td.e * a.expert_stride + (size_t)(td.m0 + r) * a.ldc + td.n0;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      float v[32];
+      if (td.nkb > 0) {
+        acc_chunk(taddr, c, v);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+      }
+      store_row_bf16_32(row + c * 32, v);
+    }
+  }
+};
+
+template <class Mode>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    plain_gemm_kernel(const __grid_constant__ TmaPair tm, const typename Mode::Args args,
+                      int ntiles, int* cursor) {
+  extern __shared__ uint8_t raw_smem[];
+  uint8_t* base = smem_aligned(raw_smem);
+  GemmSmem* S = reinterpret_cast<GemmSmem*>(base + STAGES * (A_STAGE_BYTES + B_STAGE_BYTES));
+  gemm_setup(S);
+  if (threadIdx.x == 0) S->bcast = atomicAdd(cursor, 1);
+  __syncthreads();
+  const int first = S->bcast;
+  __syncthreads();
+  gemm_roles<Mode>(args, tm, base, S, first, 0, ntiles, cursor);
+  gemm_teardown(S);
+}
+
+}  // namespace eplab_dev
+
+using namespace eplab_dev;
+
+namespace {
+int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return g_num_sms;
+}
+
+template <class Mode>
+int launch_plain(const TmaPair& tm, const typename Mode::Args& args, const TileDesc* d_tiles,
+                 int ntiles, int* d_cursor, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(plain_gemm_kernel<Mode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)GEMM_SMEM_BYTES);
+    attr = true;
+  }
+  (void)d_tiles;
+  cudaMemsetAsync(d_cursor, 0, sizeof(int), st);
+  int grid = num_sms();
+  if (grid > ntiles) grid = ntiles > 0 ? ntiles : 1;
+  plain_gemm_kernel<Mode><<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, st>>>(tm, args, ntiles, d_cursor);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+}  // namespace
+
+extern "C" {
+
+// Grouped NT GEMM over expert segments. seg_rows[e] rows of A starting at
+// seg_start[e] (multiples of 128) multiply B[e] ([N][K], K-major).
+// workspace: >= 32 B * tiles + 4 B (device). Host arrays describe the groups.
+int eplab_grouped_gemm_nt(const void* A, const void* B, void* C, int M_total, int N, int K,
+                          int n_experts, const int* seg_start, const int* seg_rows,
+                          void* d_workspace, void* stream) {
+  try {
+    std::vector<TileDesc> tiles;
+    for (int e = 0; e < n_experts; ++e)
+      for (int m = 0; m < seg_rows[e]; m += BM)
+        for (int n = 0; n < N; n += BN) {
+          TileDesc t{};
+          t.e = e;
+          t.m0 = seg_start[e] + m;
+          t.n0 = n;
+          t.rows = seg_rows[e] - m < BM ? seg_rows[e] - m : BM;
+          t.nkb = K / BK;
+          tiles.push_back(t);
+        }
+    cudaStream_t st = (cudaStream_t)stream;
+    TileDesc* d_tiles = (TileDesc*)d_workspace;
+    int* d_cursor = (int*)((char*)d_workspace + sizeof(TileDesc) * tiles.size());
+    cudaMemcpyAsync(d_tiles, tiles.data(), sizeof(TileDesc) * tiles.size(),
+                    cudaMemcpyHostToDevice, st);
+    TmaPair tm;
+    tm.a = eplab_host::make_bf16_map(A, M_total, K, K, 64, BM);
+    tm.b = eplab_host::make_bf16_map(B, (uint64_t)n_experts * N, K, K, 64, BN);
+    ModeNT::Args args{d_tiles, (__nv_bfloat16*)C, N, N};
+    return launch_plain<ModeNT>(tm, args, d_tiles, (int)tiles.size(), d_cursor, st);
+  } catch (...) {
+    return 1;
+  }
+}
+
+// Grouped TN GEMM (weight-gradient shape): C[e] ([NA][NB]) = A_seg^T * B_seg where
+// A is [M_total][NA], B is [M_total][NB] and expert e owns rows
+// [seg_start[e], seg_start[e] + seg_rows_padded[e]) (padded rows must be zero).
+int eplab_grouped_gemm_tn(const void* A, const void* B, void* C, int M_total, int NA, int NB,
+                          int n_experts, const int* seg_start, const int* seg_rows_padded,
+                          void* d_workspace, void* stream) {
+  try {
+    std::vector<TileDesc> tiles;
+    for (int e = 0; e < n_experts; ++e)
+      for (int m = 0; m < NA; m += BM)
+        for (int n = 0; n < NB; n += BN) {
+          TileDesc t{};
+          t.e = e;
+          t.m0 = m;
+          t.n0 = n;
+          t.rows = BM;
+          t.kb0 = seg_start[e];
+          t.nkb = seg_rows_padded[e] / BK;
+          tiles.push_back(t);
+        }
+    cudaStream_t st = (cudaStream_t)stream;
+    TileDesc* d_tiles = (TileDesc*)d_workspace;
+    int* d_cursor = (int*)((char*)d_workspace + sizeof(TileDesc) * tiles.size());
+    cudaMemcpyAsync(d_tiles, tiles.data(), sizeof(TileDesc) * tiles.size(),
+                    cudaMemcpyHostToDevice, st);
+    TmaPair tm;
+    tm.a = eplab_host::make_bf16_map(A, M_total, NA, NA, 64, 64);
+    tm.b = eplab_host::make_bf16_map(B, M_total, NB, NB, 64, 64);
+    ModeTN::Args args{d_tiles, (__nv_bfloat16*)C, NB, (long long)NA * NB};
+    return launch_plain<ModeTN>(tm, args, d_tiles, (int)tiles.size(), d_cursor, st);
+  } catch (...) {
+    return 1;
+  }
+}
+
+}  // extern "C"

@@ -61,6 +61,108 @@ EPLAB_API int eplab_grouped_gemm_tn(const void* d_A, const void* d_B, void* d_C,
                                     int NA, int NB, int n_experts, const int* seg_start,
                                     const int* seg_rows_padded, void* d_workspace, void* stream);
 
+
+/* ------------------------------------------------------- EP-MoE context (per rank) */
+
+typedef struct eplab_ctx eplab_ctx;
+
+/* Launch parameters chosen by the performance model (reference TuneConfig, types.hpp:45-53).
+ * n_disp: comm tasks; n_relay: relay tasks (0 = AllToAll-style, every replica sent directly;
+ * >0 = AllGather-style dedup + intra-rank multicast); n_comb: unused on B200 (the combine
+ * push is fused into the GEMM epilogue); n_red: reduce tasks; w: warps per
+ * worker (8 on B200: one 256-thread CTA per SM). */
+typedef struct {
+  int n_disp, n_relay, n_comb, n_red, w;
+} eplab_tune_config;
+
+typedef struct {
+  int rank, world, device;
+  int max_tokens;         /* tokens per rank per call (T_max) */
+  int hidden, ffn;        /* H, F (F = moe_ffn; W_up is [E_loc][2F][H]) */
+  int n_experts, topk;    /* global expert count E (sharded contiguously, e // (E/W)) */
+  long long max_recv_rows;/* 0 = worst case */
+  double timeout_s;       /* scoreboard watchdog (0 = 10 s) */
+} eplab_init_args;
+
+/* Allocates the symmetric region (receive buffers, scoreboard, replica slots, count table)
+ * and local activations for one rank on `device`. Reference analogue: the simulator state
+ * built by DispatchSim::build / CombineSim::build (sim.cpp:355-442, :767-864). */
+EPLAB_API int eplab_init(const eplab_init_args* args, eplab_ctx** out);
+EPLAB_API int eplab_destroy(eplab_ctx* ctx);
+
+/* Peer wiring. Multi-process: export my region's CUDA IPC handle (64 bytes), all-gather the
+ * handles (NCCL / torch.distributed bootstrap) and import them (world * 64 bytes, rank order).
+ * Single process (several contexts on one or more devices): link them directly. */
+EPLAB_API int eplab_ipc_handle(eplab_ctx* ctx, void* handle64);
+EPLAB_API int eplab_connect_ipc(eplab_ctx* ctx, const void* handles);
+EPLAB_API int eplab_connect_local(eplab_ctx* const* ctxs, int n);
+
+EPLAB_API int eplab_set_tune_config(eplab_ctx* ctx, const eplab_tune_config* cfg);
+EPLAB_API int eplab_get_tune_config(const eplab_ctx* ctx, eplab_tune_config* cfg);
+/* Persistent grid size (default: all SMs). Several ranks sharing one GPU (the single-device
+ * multi-rank test mode) each get a disjoint budget so their MegaKernels are co-resident. */
+EPLAB_API int eplab_set_sm_budget(eplab_ctx* ctx, int n_sm);
+
+/* Device token map (Alg. 1 + count AllGather + priority schedule), token_map.hpp:68 and :88.
+ * d_topk_ids int32 [n_tok][topk], d_gate_w fp32 [n_tok][topk]; both must stay valid until
+ * the backward calls of this iteration. Starts a new iteration (epoch). */
+EPLAB_API int eplab_plan(eplab_ctx* ctx, const int32_t* d_topk_ids, const float* d_gate_w,
+                         int n_tok, void* stream);
+
+/* Dispatch+GroupGEMM MegaKernel, forward (run_dispatch_gemm_sim, sim.hpp:87): pushes x rows to
+ * the expert ranks and runs the up GroupGEMM + SwiGLU as rowgroups land. */
+EPLAB_API int eplab_dispatch_group_gemm(eplab_ctx* ctx, const void* d_x, const void* d_w_up,
+                                        void* stream);
+/* GroupGEMM+Combine MegaKernel, forward (run_gemm_combine_sim, sim.hpp:88 + accumulate,
+ * precision.hpp:30): down GroupGEMM whose epilogue pushes each replica to its source, then
+ * the top-k barrier and the k-ordered reduction into d_y [n_tok][H] bf16. */
+EPLAB_API int eplab_group_gemm_combine(eplab_ctx* ctx, const void* d_w_down, void* d_y,
+                                       void* stream);
+/* Backward Dispatch+GroupGEMM: dY dispatch, gate gradient, down dgrad + SwiGLU backward,
+ * down weight gradient (deterministic transposed GroupGEMM). */
+EPLAB_API int eplab_dispatch_group_gemm_bwd(eplab_ctx* ctx, const void* d_dy,
+                                            const void* d_w_down, void* d_dw_down,
+                                            float* d_dgate, void* stream);
+/* Backward GroupGEMM+Combine: up dgrad pushed back and k-reduced into d_dx, up weight grad. */
+EPLAB_API int eplab_group_gemm_combine_bwd(eplab_ctx* ctx, const void* d_w_up, void* d_dx,
+                                           void* d_dw_up, void* stream);
+
+/* Whole layer. fwd = plan + the two forward MegaKernels; bwd = the two backward ones. */
+EPLAB_API int eplab_moe_fwd(eplab_ctx* ctx, const int32_t* d_topk_ids, const float* d_gate_w,
+                            int n_tok, const void* d_x, const void* d_w_up, const void* d_w_down,
+                            void* d_y, void* stream);
+EPLAB_API int eplab_moe_bwd(eplab_ctx* ctx, const void* d_dy, const void* d_w_up,
+                            const void* d_w_down, void* d_dx, void* d_dw_up, void* d_dw_down,
+                            float* d_dgate, void* stream);
+/* fwd+bwd with HOST routing/activations (pinned or pageable): H2D copies, the four
+ * MegaKernels, D2H of y, dx and dgate, all on `stream`; synchronises before returning. */
+EPLAB_API int eplab_moe_step_host(eplab_ctx* ctx, const int32_t* h_topk_ids,
+                                  const float* h_gate_w, int n_tok, const void* h_x,
+                                  const void* h_dy, const void* d_w_up, const void* d_w_down,
+                                  void* h_y, void* h_dx, float* h_dgate, void* d_dw_up,
+                                  void* d_dw_down, void* stream);
+
+/* Synchronises `stream` and reports the device error word: 0 ok, 2 capacity exceeded,
+ * 3 scoreboard watchdog fired (DeadlockError analogue, error.hpp:19-22). Clears it. */
+EPLAB_API int eplab_check(eplab_ctx* ctx, void* stream);
+
+/* Bit-exact exports of the device token map (synchronising). Arrays of n_tok*topk entries;
+ * recv_totals / seg_base have world*epr entries (GlobalTokenMap, token_map.hpp:52-66). */
+EPLAB_API int eplab_export_token_map(eplab_ctx* ctx, int32_t* target_rank, int32_t* local_expert,
+                                     int64_t* offset, int64_t* recv_totals, int64_t* seg_base);
+/* Priority send schedule (SendSchedule, token_map.hpp:70-88): token and k-slot per item. */
+EPLAB_API int eplab_export_schedule(eplab_ctx* ctx, int64_t* item_token, int32_t* item_slot);
+/* Receive-side geometry actually used: 128-aligned segment base and rows per local expert. */
+EPLAB_API int eplab_export_layout(eplab_ctx* ctx, int32_t* seg_base_aligned, int32_t* rows);
+/* Device pointer of a named internal buffer (tests / profiling): "recv_x", "recv_dy", "gu",
+ * "hact", "dgu", "hw", "rep", "rep_dx". */
+EPLAB_API void* eplab_buffer(eplab_ctx* ctx, const char* name);
+
+/* Device timeline (per-task %globaltimer intervals, role, SM) for overlap analysis, exported in
+ * the reference's Chrome-trace format (trace.cpp:13-34). cap = 0 disables. */
+EPLAB_API int eplab_timeline_enable(eplab_ctx* ctx, int cap);
+EPLAB_API int eplab_timeline_export(eplab_ctx* ctx, const char* path, double* overlap_frac);
+
 #ifdef __cplusplus
 }
 #endif

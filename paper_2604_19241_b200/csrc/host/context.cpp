@@ -1,0 +1,661 @@
+// Per-rank EP-MoE context: symmetric-region allocation and peer wiring, the device token map
+// launch, MegaKernel orchestration and the C-ABI data path (include/eplab_b200.h).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "eplab_b200.h"
+#include "host/errors.hpp"
+#include "host/launch.hpp"
+#include "kernels/tma_host.hpp"
+
+using namespace eplab_dev;
+
+namespace {
+
+constexpr int kBM = 128;
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+#define CK(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess) throw Fail{EPLAB_ERR_INTERNAL, std::string(#call) + ": " +  \
+                                               cudaGetErrorString(e_)};                \
+  } while (0)
+
+}  // namespace
+
+struct eplab_ctx {
+  Dims d{};
+  int device = 0;
+  int num_sms = 148;
+  unsigned long long timeout_ns = 10'000'000'000ULL;
+  // symmetric region
+  char* sym = nullptr;
+  size_t sym_bytes = 0;
+  size_t off_recv_x = 0, off_recv_dy = 0, off_meta = 0, off_slot_flag = 0, off_rg = 0, off_rep = 0,
+         off_rep_dx = 0, off_tok = 0, off_cnt_all = 0, off_cnt_flag = 0;
+  SymPtrs mine{};
+  Peers peers{};
+  std::vector<void*> ipc_opened;
+  // local region
+  char* loc = nullptr;
+  PlanDev plan{};
+  __nv_bfloat16 *gu = nullptr, *hact = nullptr, *dgu = nullptr, *hw = nullptr;
+  uint32_t* wg_cnt = nullptr;
+  int* cursor = nullptr;
+  int* err = nullptr;
+  // host-call staging (eplab_moe_step_host)
+  char* stage = nullptr;
+  // fixed tensor maps
+  CUtensorMap tm_recv_x_k{}, tm_recv_x_mn{}, tm_hact_k{}, tm_recv_dy_k{}, tm_recv_dy_mn{},
+      tm_hw_mn{}, tm_dgu_k{}, tm_dgu_mn{};
+  // iteration state
+  uint32_t epoch = 0;
+  bool planned = false;
+  eplab_tune_config cfg{32, 0, 0, 148, 8};
+  // timeline
+  TimelineRec* tl_rec = nullptr;
+  int* tl_count = nullptr;
+  int tl_cap = 0;
+};
+
+namespace {
+
+SymPtrs sym_ptrs(const eplab_ctx* c, char* base) {
+  SymPtrs s;
+  s.recv_x = reinterpret_cast<__nv_bfloat16*>(base + c->off_recv_x);
+  s.recv_dy = reinterpret_cast<__nv_bfloat16*>(base + c->off_recv_dy);
+  s.meta = reinterpret_cast<SlotMeta*>(base + c->off_meta);
+  s.slot_flag = reinterpret_cast<uint32_t*>(base + c->off_slot_flag);
+  s.rg_cnt = reinterpret_cast<uint32_t*>(base + c->off_rg);
+  s.rep = reinterpret_cast<__nv_bfloat16*>(base + c->off_rep);
+  s.rep_dx = reinterpret_cast<__nv_bfloat16*>(base + c->off_rep_dx);
+  s.tok_cnt = reinterpret_cast<uint32_t*>(base + c->off_tok);
+  s.cnt_all = reinterpret_cast<int*>(base + c->off_cnt_all);
+  s.cnt_flag = reinterpret_cast<uint32_t*>(base + c->off_cnt_flag);
+  return s;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return EPLAB_OK;
+  } catch (const Fail& e) {
+    eplab_host::set_last_error(e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    eplab_host::set_last_error(e.what());
+    return EPLAB_ERR_INTERNAL;
+  }
+}
+
+void validate(bool ok, const std::string& msg) {
+  if (!ok) throw Fail{EPLAB_ERR_VALIDATION, msg};
+}
+
+MkArgs base_args(eplab_ctx* c) {
+  MkArgs a{};
+  a.d = c->d;
+  a.peers = c->peers;
+  a.p = c->plan;
+  a.gu = c->gu;
+  a.hact = c->hact;
+  a.dgu = c->dgu;
+  a.hw = c->hw;
+  a.wg_cnt = c->wg_cnt;
+  a.cursor = c->cursor;
+  a.err = c->err;
+  a.epoch = c->epoch;
+  a.par = (int)(c->epoch & 1);
+  a.n_disp = std::max(1, c->cfg.n_disp);
+  a.n_relay = std::max(0, c->cfg.n_relay);
+  a.n_red = std::max(1, c->cfg.n_red);
+  a.timeout_ns = c->timeout_ns;
+  a.tl = Timeline{c->tl_rec, c->tl_count, c->tl_cap};
+  return a;
+}
+
+void require_plan(eplab_ctx* c) {
+  validate(c->planned, "no plan: call eplab_plan (or eplab_moe_fwd) first");
+}
+
+}  // namespace
+
+extern "C" {
+
+int eplab_init(const eplab_init_args* args, eplab_ctx** out) {
+  return guarded([&] {
+    validate(args && out, "null argument");
+    const int W = args->world, E = args->n_experts, k = args->topk;
+    validate(W >= 1 && W <= MAX_WORLD, "world must be in [1, 8]");
+    validate(args->rank >= 0 && args->rank < W, "rank out of range");
+    validate(E >= 1 && E <= MAX_EXPERTS, "n_experts must be in [1, 512]");
+    validate(E % W == 0, "n_experts not divisible by world");
+    validate(k >= 1 && k <= 16 && k <= E, "topk must be in [1, min(16, n_experts)]");
+    validate(args->hidden > 0 && args->hidden % 256 == 0, "hidden must be a multiple of 256");
+    validate(args->ffn > 0 && args->ffn % 256 == 0, "ffn must be a multiple of 256");
+    validate(args->max_tokens > 0, "max_tokens must be > 0");
+    auto* c = new eplab_ctx();
+    c->device = args->device;
+    CK(cudaSetDevice(c->device));
+    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+    if (args->timeout_s > 0) c->timeout_ns = (unsigned long long)(args->timeout_s * 1e9);
+    Dims& d = c->d;
+    d.H = args->hidden;
+    d.F = args->ffn;
+    d.E = E;
+    d.epr = E / W;
+    d.topk = k;
+    d.world = W;
+    d.rank = args->rank;
+    d.T_max = args->max_tokens;
+    long long worst = (long long)W * d.T_max * std::min(k, d.epr) + (long long)d.epr * 127;
+    long long mcap = args->max_recv_rows > 0 ? args->max_recv_rows + (long long)d.epr * 127 : worst;
+    mcap = (long long)align_up((size_t)mcap, kBM);
+    validate(mcap < (1LL << 31) / 2, "receive capacity too large");
+    d.M_cap = (int)mcap;
+    d.RG_cap = d.M_cap / kBM;
+    c->cfg.n_red = c->num_sms;
+
+    // ---- symmetric region
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+      size_t at = o;
+      o = align_up(o + bytes, 256);
+      return at;
+    };
+    const size_t M = d.M_cap, Tk = (size_t)d.T_max * k;
+    c->off_recv_x = take(M * d.H * 2);
+    c->off_recv_dy = take(M * d.H * 2);
+    c->off_meta = take(M * sizeof(SlotMeta));
+    c->off_slot_flag = take(M * 4);
+    c->off_rg = take((size_t)4 * d.RG_cap * 4);
+    c->off_rep = take(Tk * d.H * 2);
+    c->off_rep_dx = take(Tk * d.H * 2);
+    c->off_tok = take((size_t)4 * d.T_max * 4);
+    c->off_cnt_all = take((size_t)W * E * 4);
+    c->off_cnt_flag = take((size_t)W * 4);
+    c->sym_bytes = o;
+    CK(cudaMalloc(&c->sym, c->sym_bytes));
+    CK(cudaMemset(c->sym + c->off_meta, 0, o - c->off_meta));
+    c->mine = sym_ptrs(c, c->sym);
+    for (int r = 0; r < MAX_WORLD; ++r) c->peers.p[r] = c->mine;  // until connected
+
+    // ---- local region
+    const int nchunks = (int)((Tk + PLAN_CHUNK - 1) / PLAN_CHUNK) + 1;
+    o = 0;
+    const size_t o_gu = take(M * 2 * d.F * 2), o_h = take(M * d.F * 2), o_dgu = take(M * 2 * d.F * 2),
+                 o_hw = take(M * d.F * 2), o_hist = take((size_t)nchunks * E * 4),
+                 o_counts = take(E * 4), o_sb = take(E * 4), o_oall = take(E * 4),
+                 o_bb = take(E * 4), o_dslot = take(Tk * 4), o_off = take(Tk * 4),
+                 o_sched = take(Tk * 4), o_rt = take((size_t)W * d.epr * 4),
+                 o_sbr = take((size_t)W * d.epr * 4), o_sba = take((size_t)W * d.epr * 4),
+                 o_mb = take(d.epr * 4), o_mbp = take((d.epr + 1) * 4), o_sc = take(64),
+                 o_wg = take((size_t)d.epr * (d.F / 256) * 4), o_cur = take(64), o_err = take(64);
+    CK(cudaMalloc(&c->loc, o));
+    CK(cudaMemset(c->loc + o_hist, 0, o - o_hist));
+    c->gu = reinterpret_cast<__nv_bfloat16*>(c->loc + o_gu);
+    c->hact = reinterpret_cast<__nv_bfloat16*>(c->loc + o_h);
+    c->dgu = reinterpret_cast<__nv_bfloat16*>(c->loc + o_dgu);
+    c->hw = reinterpret_cast<__nv_bfloat16*>(c->loc + o_hw);
+    PlanDev& p = c->plan;
+    p.hist = reinterpret_cast<int*>(c->loc + o_hist);
+    p.counts = reinterpret_cast<int*>(c->loc + o_counts);
+    p.send_base = reinterpret_cast<int*>(c->loc + o_sb);
+    p.o_all = reinterpret_cast<int*>(c->loc + o_oall);
+    p.bucket_base = reinterpret_cast<int*>(c->loc + o_bb);
+    p.dst_slot = reinterpret_cast<int*>(c->loc + o_dslot);
+    p.offset = reinterpret_cast<int*>(c->loc + o_off);
+    p.sched = reinterpret_cast<int*>(c->loc + o_sched);
+    p.rt_all = reinterpret_cast<int*>(c->loc + o_rt);
+    p.sb_all_ref = reinterpret_cast<int*>(c->loc + o_sbr);
+    p.sb_all = reinterpret_cast<int*>(c->loc + o_sba);
+    p.mblocks = reinterpret_cast<int*>(c->loc + o_mb);
+    p.mblock_pre = reinterpret_cast<int*>(c->loc + o_mbp);
+    p.scalars = reinterpret_cast<int*>(c->loc + o_sc);
+    c->wg_cnt = reinterpret_cast<uint32_t*>(c->loc + o_wg);
+    c->cursor = reinterpret_cast<int*>(c->loc + o_cur);
+    c->err = reinterpret_cast<int*>(c->loc + o_err);
+
+    // ---- host-call staging: ids, gate weights, x, dy, y, dx, dgate
+    o = 0;
+    take(Tk * 4);
+    take(Tk * 4);
+    take((size_t)d.T_max * d.H * 2);
+    take((size_t)d.T_max * d.H * 2);
+    take((size_t)d.T_max * d.H * 2);
+    take((size_t)d.T_max * d.H * 2);
+    take(Tk * 4);
+    CK(cudaMalloc(&c->stage, o));
+
+    // ---- fixed tensor maps
+    using eplab_host::make_bf16_map;
+    const SymPtrs& s = c->mine;
+    c->tm_recv_x_k = make_bf16_map(s.recv_x, M, d.H, d.H, 64, 128);
+    c->tm_recv_x_mn = make_bf16_map(s.recv_x, M, d.H, d.H, 64, 64);
+    c->tm_recv_dy_k = make_bf16_map(s.recv_dy, M, d.H, d.H, 64, 128);
+    c->tm_recv_dy_mn = make_bf16_map(s.recv_dy, M, d.H, d.H, 64, 64);
+    c->tm_hact_k = make_bf16_map(c->hact, M, d.F, d.F, 64, 128);
+    c->tm_hw_mn = make_bf16_map(c->hw, M, d.F, d.F, 64, 64);
+    c->tm_dgu_k = make_bf16_map(c->dgu, M, 2 * d.F, 2 * d.F, 64, 128);
+    c->tm_dgu_mn = make_bf16_map(c->dgu, M, 2 * d.F, 2 * d.F, 64, 64);
+    CK(cudaDeviceSynchronize());
+    *out = c;
+  });
+}
+
+int eplab_destroy(eplab_ctx* c) {
+  if (!c) return EPLAB_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  cudaFree(c->sym);
+  cudaFree(c->loc);
+  cudaFree(c->stage);
+  if (c->tl_rec) cudaFree(c->tl_rec);
+  if (c->tl_count) cudaFree(c->tl_count);
+  delete c;
+  return EPLAB_OK;
+}
+
+int eplab_ipc_handle(eplab_ctx* c, void* handle64) {
+  return guarded([&] {
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, c->sym));
+    static_assert(sizeof(h) == 64, "ipc handle size");
+    std::memcpy(handle64, &h, 64);
+  });
+}
+
+int eplab_connect_ipc(eplab_ctx* c, const void* handles) {
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    const char* hs = static_cast<const char*>(handles);
+    for (int r = 0; r < c->d.world; ++r) {
+      if (r == c->d.rank) {
+        c->peers.p[r] = c->mine;
+        continue;
+      }
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, hs + 64 * r, 64);
+      void* p = nullptr;
+      CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      c->ipc_opened.push_back(p);
+      c->peers.p[r] = sym_ptrs(c, static_cast<char*>(p));
+    }
+  });
+}
+
+int eplab_connect_local(eplab_ctx* const* ctxs, int n) {
+  return guarded([&] {
+    validate(n >= 1 && n <= MAX_WORLD, "bad context count");
+    for (int i = 0; i < n; ++i) {
+      validate(ctxs[i]->d.world == n && ctxs[i]->d.rank == i, "contexts must be ranks 0..n-1");
+      validate(ctxs[i]->sym_bytes == ctxs[0]->sym_bytes, "contexts must be symmetric");
+    }
+    for (int i = 0; i < n; ++i) {
+      cudaSetDevice(ctxs[i]->device);
+      for (int j = 0; j < n; ++j) {
+        if (ctxs[j]->device != ctxs[i]->device) {
+          cudaError_t e = cudaDeviceEnablePeerAccess(ctxs[j]->device, 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+            throw Fail{EPLAB_ERR_INTERNAL, "peer access unavailable"};
+          cudaGetLastError();
+        }
+        ctxs[i]->peers.p[j] = ctxs[j]->mine;
+      }
+    }
+  });
+}
+
+int eplab_set_tune_config(eplab_ctx* c, const eplab_tune_config* cfg) {
+  return guarded([&] {
+    validate(cfg->w == 8 || cfg->w == 16 || cfg->w == 32, "w must be one of {8,16,32}");
+    validate(cfg->n_disp >= 1, "n_disp must be >= 1");
+    validate(cfg->n_relay >= 0, "n_relay must be >= 0");
+    // deadlock constraint of types.cpp:59-64; producers are claimed first, so the persistent
+    // grid (one CTA per SM) always keeps at least one SM for compute.
+    validate(cfg->n_disp + cfg->n_relay < c->num_sms,
+             "n_disp + n_relay must be < n_sm (deadlock constraint)");
+    validate(cfg->n_red >= 1 && cfg->n_red <= c->num_sms, "n_red must be in [1, n_sm]");
+    c->cfg = *cfg;
+  });
+}
+
+int eplab_set_sm_budget(eplab_ctx* c, int n_sm) {
+  return guarded([&] {
+    int dev_sms = 0;
+    CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device));
+    validate(n_sm >= 2 && n_sm <= dev_sms, "sm budget must be in [2, device SMs]");
+    c->num_sms = n_sm;
+    c->cfg.n_red = std::min(c->cfg.n_red, n_sm);
+    if (c->cfg.n_disp + c->cfg.n_relay >= n_sm) {
+      c->cfg.n_disp = std::max(1, n_sm / 4);
+      c->cfg.n_relay = c->cfg.n_relay ? 1 : 0;
+    }
+  });
+}
+
+int eplab_get_tune_config(const eplab_ctx* c, eplab_tune_config* cfg) {
+  *cfg = c->cfg;
+  return EPLAB_OK;
+}
+
+int eplab_plan(eplab_ctx* c, const int32_t* ids, const float* gw, int n_tok, void* stream) {
+  return guarded([&] {
+    validate(n_tok >= 0 && n_tok <= c->d.T_max, "n_tok exceeds max_tokens");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    c->epoch++;
+    c->plan.n_tok = n_tok;
+    c->plan.topk_ids = ids;
+    c->plan.gate_w = gw;
+    if (eplab_launch::plan_launch(c->d, c->peers, c->plan, c->epoch, c->timeout_ns, c->err, st))
+      throw Fail{EPLAB_ERR_INTERNAL, std::string("plan launch: ") +
+                                         cudaGetErrorString(cudaGetLastError())};
+    eplab_launch::zero_padding_launch(c->d, c->plan, c->mine.recv_x, st);
+    eplab_launch::zero_padding_launch(c->d, c->plan, c->mine.recv_dy, st);
+    CK(cudaGetLastError());
+    c->planned = true;
+  });
+}
+
+int eplab_dispatch_group_gemm(eplab_ctx* c, const void* x, const void* w_up, void* stream) {
+  return guarded([&] {
+    require_plan(c);
+    CK(cudaSetDevice(c->device));
+    MkArgs a = base_args(c);
+    a.x = static_cast<const __nv_bfloat16*>(x);
+    a.w_up = static_cast<const __nv_bfloat16*>(w_up);
+    TmaSet tm;
+    tm.m[0] = c->tm_recv_x_k;
+    tm.m[1] = eplab_host::make_bf16_map(w_up, (uint64_t)c->d.epr * 2 * c->d.F, c->d.H, c->d.H, 64, 128);
+    tm.m[2] = tm.m[0];
+    tm.m[3] = tm.m[1];
+    if (eplab_launch::launch_fwd_dispatch(tm, a, c->num_sms, (cudaStream_t)stream))
+      throw Fail{EPLAB_ERR_INTERNAL, std::string("dispatch launch: ") +
+                                         cudaGetErrorString(cudaGetLastError())};
+  });
+}
+
+int eplab_group_gemm_combine(eplab_ctx* c, const void* w_down, void* y, void* stream) {
+  return guarded([&] {
+    require_plan(c);
+    CK(cudaSetDevice(c->device));
+    MkArgs a = base_args(c);
+    a.w_down = static_cast<const __nv_bfloat16*>(w_down);
+    a.y = static_cast<__nv_bfloat16*>(y);
+    TmaSet tm;
+    tm.m[0] = c->tm_hact_k;
+    tm.m[1] = eplab_host::make_bf16_map(w_down, (uint64_t)c->d.epr * c->d.H, c->d.F, c->d.F, 64, 256);
+    tm.m[2] = tm.m[0];
+    tm.m[3] = tm.m[1];
+    if (eplab_launch::launch_fwd_combine(tm, a, c->num_sms, (cudaStream_t)stream))
+      throw Fail{EPLAB_ERR_INTERNAL, std::string("combine launch: ") +
+                                         cudaGetErrorString(cudaGetLastError())};
+  });
+}
+
+int eplab_dispatch_group_gemm_bwd(eplab_ctx* c, const void* dy, const void* w_down, void* dw_down,
+                                  float* dgate, void* stream) {
+  return guarded([&] {
+    require_plan(c);
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaMemsetAsync(c->wg_cnt, 0, (size_t)c->d.epr * (c->d.F / 256) * 4, st));
+    MkArgs a = base_args(c);
+    a.dy = static_cast<const __nv_bfloat16*>(dy);
+    a.w_down = static_cast<const __nv_bfloat16*>(w_down);
+    a.dw_down = static_cast<__nv_bfloat16*>(dw_down);
+    a.dgate = dgate;
+    TmaSet tm;
+    tm.m[0] = c->tm_recv_dy_k;
+    tm.m[1] = eplab_host::make_bf16_map(w_down, (uint64_t)c->d.epr * c->d.H, c->d.F, c->d.F, 64, 64);
+    tm.m[2] = c->tm_recv_dy_mn;
+    tm.m[3] = c->tm_hw_mn;
+    if (eplab_launch::launch_bwd_dispatch(tm, a, c->num_sms, st))
+      throw Fail{EPLAB_ERR_INTERNAL, std::string("bwd dispatch launch: ") +
+                                         cudaGetErrorString(cudaGetLastError())};
+  });
+}
+
+int eplab_group_gemm_combine_bwd(eplab_ctx* c, const void* w_up, void* dx, void* dw_up,
+                                 void* stream) {
+  return guarded([&] {
+    require_plan(c);
+    CK(cudaSetDevice(c->device));
+    MkArgs a = base_args(c);
+    a.w_up = static_cast<const __nv_bfloat16*>(w_up);
+    a.dx = static_cast<__nv_bfloat16*>(dx);
+    a.dw_up = static_cast<__nv_bfloat16*>(dw_up);
+    TmaSet tm;
+    tm.m[0] = c->tm_dgu_k;
+    tm.m[1] = eplab_host::make_bf16_map(w_up, (uint64_t)c->d.epr * 2 * c->d.F, c->d.H, c->d.H, 64, 64);
+    tm.m[2] = c->tm_dgu_mn;
+    tm.m[3] = c->tm_recv_x_mn;
+    if (eplab_launch::launch_bwd_combine(tm, a, c->num_sms, (cudaStream_t)stream))
+      throw Fail{EPLAB_ERR_INTERNAL, std::string("bwd combine launch: ") +
+                                         cudaGetErrorString(cudaGetLastError())};
+  });
+}
+
+int eplab_moe_fwd(eplab_ctx* c, const int32_t* ids, const float* gw, int n_tok, const void* x,
+                  const void* w_up, const void* w_down, void* y, void* stream) {
+  int rc = eplab_plan(c, ids, gw, n_tok, stream);
+  if (!rc) rc = eplab_dispatch_group_gemm(c, x, w_up, stream);
+  if (!rc) rc = eplab_group_gemm_combine(c, w_down, y, stream);
+  return rc;
+}
+
+int eplab_moe_bwd(eplab_ctx* c, const void* dy, const void* w_up, const void* w_down, void* dx,
+                  void* dw_up, void* dw_down, float* dgate, void* stream) {
+  int rc = eplab_dispatch_group_gemm_bwd(c, dy, w_down, dw_down, dgate, stream);
+  if (!rc) rc = eplab_group_gemm_combine_bwd(c, w_up, dx, dw_up, stream);
+  return rc;
+}
+
+int eplab_moe_step_host(eplab_ctx* c, const int32_t* h_ids, const float* h_gw, int n_tok,
+                        const void* h_x, const void* h_dy, const void* w_up, const void* w_down,
+                        void* h_y, void* h_dx, float* h_dgate, void* dw_up, void* dw_down,
+                        void* stream) {
+  int rc = guarded([&] {
+    validate(n_tok >= 0 && n_tok <= c->d.T_max, "n_tok exceeds max_tokens");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t Tk = (size_t)c->d.T_max * c->d.topk, TH = (size_t)c->d.T_max * c->d.H * 2;
+    char* s = c->stage;
+    int32_t* ids = reinterpret_cast<int32_t*>(s);
+    float* gw = reinterpret_cast<float*>(s + align_up(Tk * 4, 256));
+    char* x = s + 2 * align_up(Tk * 4, 256);
+    char* dy = x + align_up(TH, 256);
+    char* y = dy + align_up(TH, 256);
+    char* dx = y + align_up(TH, 256);
+    float* dg = reinterpret_cast<float*>(dx + align_up(TH, 256));
+    const size_t nk = (size_t)n_tok * c->d.topk, nh = (size_t)n_tok * c->d.H * 2;
+    CK(cudaMemcpyAsync(ids, h_ids, nk * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(gw, h_gw, nk * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(x, h_x, nh, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dy, h_dy, nh, cudaMemcpyHostToDevice, st));
+    int r = eplab_moe_fwd(c, ids, gw, n_tok, x, w_up, w_down, y, stream);
+    if (!r) r = eplab_moe_bwd(c, dy, w_up, w_down, dx, dw_up, dw_down, dg, stream);
+    if (r) throw Fail{r, eplab_host::last_error()};
+    CK(cudaMemcpyAsync(h_y, y, nh, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_dx, dx, nh, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_dgate, dg, nk * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+  return rc;
+}
+
+int eplab_check(eplab_ctx* c, void* stream) {
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    int ev[8] = {0};
+    CK(cudaMemcpy(ev, c->err, sizeof(ev), cudaMemcpyDeviceToHost));
+    CK(cudaMemset(c->err, 0, sizeof(ev)));
+    const int e = ev[0];
+    if (e == 3)
+      throw Fail{EPLAB_ERR_DEADLOCK,
+                 "DeadlockDetected: scoreboard watchdog fired (site " + std::to_string(ev[1]) +
+                     ", target " + std::to_string(ev[2]) + ", seen " + std::to_string(ev[3]) +
+                     ", at " + std::to_string(ev[4]) + ")"};
+    if (e == 2) throw Fail{EPLAB_ERR_VALIDATION, "receive capacity exceeded (max_recv_rows)"};
+    if (e) throw Fail{EPLAB_ERR_INTERNAL, "device error word " + std::to_string(e)};
+  });
+}
+
+int eplab_export_token_map(eplab_ctx* c, int32_t* target_rank, int32_t* local_expert,
+                           int64_t* offset, int64_t* recv_totals, int64_t* seg_base) {
+  return guarded([&] {
+    require_plan(c);
+    CK(cudaSetDevice(c->device));
+    CK(cudaDeviceSynchronize());
+    const int n = c->plan.n_tok * c->d.topk, Wepr = c->d.world * c->d.epr;
+    std::vector<int32_t> ids(n), off(n), rt(Wepr), sb(Wepr);
+    if (n) {
+      CK(cudaMemcpy(ids.data(), c->plan.topk_ids, n * 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(off.data(), c->plan.offset, n * 4, cudaMemcpyDeviceToHost));
+    }
+    CK(cudaMemcpy(rt.data(), c->plan.rt_all, Wepr * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(sb.data(), c->plan.sb_all_ref, Wepr * 4, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i) {
+      if (target_rank) target_rank[i] = ids[i] / c->d.epr;
+      if (local_expert) local_expert[i] = ids[i] % c->d.epr;
+      if (offset) offset[i] = off[i];
+    }
+    for (int i = 0; i < Wepr; ++i) {
+      if (recv_totals) recv_totals[i] = rt[i];
+      if (seg_base) seg_base[i] = sb[i];
+    }
+  });
+}
+
+int eplab_export_schedule(eplab_ctx* c, int64_t* item_token, int32_t* item_slot) {
+  return guarded([&] {
+    require_plan(c);
+    CK(cudaSetDevice(c->device));
+    CK(cudaDeviceSynchronize());
+    const int n = c->plan.n_tok * c->d.topk;
+    std::vector<int32_t> s(n);
+    if (n) CK(cudaMemcpy(s.data(), c->plan.sched, n * 4, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i) {
+      item_token[i] = s[i] / c->d.topk;
+      item_slot[i] = s[i] % c->d.topk;
+    }
+  });
+}
+
+int eplab_export_layout(eplab_ctx* c, int32_t* seg_base_aligned, int32_t* rows) {
+  return guarded([&] {
+    require_plan(c);
+    CK(cudaSetDevice(c->device));
+    CK(cudaDeviceSynchronize());
+    const int off = c->d.rank * c->d.epr;
+    CK(cudaMemcpy(seg_base_aligned, c->plan.sb_all + off, c->d.epr * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(rows, c->plan.rt_all + off, c->d.epr * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+void* eplab_buffer(eplab_ctx* c, const char* name) {
+  const std::string n(name);
+  if (n == "recv_x") return c->mine.recv_x;
+  if (n == "recv_dy") return c->mine.recv_dy;
+  if (n == "gu") return c->gu;
+  if (n == "hact") return c->hact;
+  if (n == "dgu") return c->dgu;
+  if (n == "hw") return c->hw;
+  if (n == "rep") return c->mine.rep;
+  if (n == "rep_dx") return c->mine.rep_dx;
+  return nullptr;
+}
+
+int eplab_timeline_enable(eplab_ctx* c, int cap) {
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    if (c->tl_rec) cudaFree(c->tl_rec);
+    if (c->tl_count) cudaFree(c->tl_count);
+    c->tl_rec = nullptr;
+    c->tl_count = nullptr;
+    c->tl_cap = 0;
+    if (cap <= 0) return;
+    CK(cudaMalloc(&c->tl_rec, sizeof(TimelineRec) * (size_t)cap));
+    CK(cudaMalloc(&c->tl_count, 4));
+    CK(cudaMemset(c->tl_count, 0, 4));
+    c->tl_cap = cap;
+  });
+}
+
+// Chrome trace (reference trace.cpp:13-34 field names: name/cat/ph/ts/dur/pid/tid/args) and the
+// overlap fraction = |comm-or-relay active AND comp active| / |comm-or-relay active|.
+int eplab_timeline_export(eplab_ctx* c, const char* path, double* overlap_frac) {
+  return guarded([&] {
+    validate(c->tl_rec != nullptr, "timeline not enabled");
+    CK(cudaSetDevice(c->device));
+    CK(cudaDeviceSynchronize());
+    int n = 0;
+    CK(cudaMemcpy(&n, c->tl_count, 4, cudaMemcpyDeviceToHost));
+    n = std::min(n, c->tl_cap);
+    std::vector<TimelineRec> r(n);
+    if (n) CK(cudaMemcpy(r.data(), c->tl_rec, sizeof(TimelineRec) * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemset(c->tl_count, 0, 4));
+    unsigned long long t0 = ~0ULL;
+    for (auto& x : r) t0 = std::min(t0, x.t0);
+    static const char* names[4] = {"comm", "relay", "comp", "reduce"};
+    if (path && *path) {
+      std::ofstream f(path);
+      if (!f) throw Fail{EPLAB_ERR_VALIDATION, std::string("cannot write ") + path};
+      f << "{\"traceEvents\": [\n";
+      for (int i = 0; i < n; ++i) {
+        const uint32_t role = r[i].sm_role >> 16, sm = r[i].sm_role & 0xFFFF;
+        f << (i ? ",\n" : "") << "{\"name\": \"" << names[role & 3] << "\", \"cat\": \""
+          << names[role & 3] << "\", \"ph\": \"X\", \"ts\": " << (r[i].t0 - t0) * 1e-3
+          << ", \"dur\": " << (r[i].t1 - r[i].t0) * 1e-3 << ", \"pid\": " << c->d.rank
+          << ", \"tid\": " << sm << ", \"args\": {\"task\": " << r[i].task << "}}";
+      }
+      f << "\n], \"displayTimeUnit\": \"ns\"}\n";
+    }
+    if (overlap_frac) {
+      // sweep over interval endpoints
+      std::vector<std::pair<unsigned long long, int>> ev;  // (time, +-1 comm | +-2 comp)
+      for (auto& x : r) {
+        const uint32_t role = x.sm_role >> 16;
+        const int kind = (role == ROLE_COMM || role == ROLE_RELAY) ? 1 : (role == ROLE_COMP ? 2 : 0);
+        if (!kind) continue;
+        ev.push_back({x.t0, kind});
+        ev.push_back({x.t1, -kind});
+      }
+      std::sort(ev.begin(), ev.end());
+      long long comm = 0, comp = 0;
+      unsigned long long last = ev.empty() ? 0 : ev[0].first;
+      double t_comm = 0, t_both = 0;
+      for (auto& e : ev) {
+        const double dt = (double)(e.first - last);
+        if (comm > 0) t_comm += dt;
+        if (comm > 0 && comp > 0) t_both += dt;
+        last = e.first;
+        if (e.second == 1) ++comm;
+        if (e.second == -1) --comm;
+        if (e.second == 2) ++comp;
+        if (e.second == -2) --comp;
+      }
+      *overlap_frac = t_comm > 0 ? t_both / t_comm : 0.0;
+    }
+  });
+}
+
+}  // extern "C"

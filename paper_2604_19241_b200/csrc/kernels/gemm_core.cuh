@@ -53,6 +53,7 @@ struct GemmSmem {
   uint64_t tempty[ACC_STAGES];
   uint64_t rfull[RING];
   uint64_t rempty[RING];
+  unsigned long long tstart[8];
   int ring[RING];
   uint32_t tmem_base;
   int bcast;

@@ -1,29 +1,40 @@
 // The warp-specialised role loop of the grouped-GEMM engine (see gemm_core.cuh).
-// Mode supplies operand majors, the per-tile TMA coordinates and the epilogue.
+// Mode supplies, per tile: operand majors, TMA coordinates, an optional wait before
+// the loads (scoreboard), the epilogue and a tile-done hook.
 #pragma once
 #include "gemm_core.cuh"
+#include "moe_common.cuh"
 
 namespace eplab_dev {
 
-// Tensor maps travel as __grid_constant__ kernel parameters.
-struct TmaPair {
-  CUtensorMap a;
-  CUtensorMap b;
-};
+__device__ __forceinline__ void timeline_push(const Timeline& tl, unsigned long long t0,
+                                              unsigned long long t1, uint32_t role, int task) {
+  if (!tl.rec) return;
+  const int i = atomicAdd(tl.count, 1);
+  if (i < tl.cap) {
+    TimelineRec r;
+    r.t0 = t0;
+    r.t1 = t1;
+    r.sm_role = smid() | (role << 16);
+    r.task = task;
+    r.pad[0] = r.pad[1] = 0;
+    tl.rec[i] = r;
+  }
+}
 
-// Called once per CTA after barriers/TMEM are set up. `first` is the first
-// tile task (already claimed by the CTA while it was resolving pre-tasks).
-// Returns the first task id claimed that lies beyond the tile range
-// (so the caller can continue with post-tasks), or TASK_STOP.
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// Called once per CTA after barriers/TMEM are set up. `first` is the first tile
+// task (already claimed by the CTA while it resolved pre-tasks). Returns the first
+// claimed id beyond [tile_lo, tile_hi) so the caller can continue with post-tasks.
 template <class Mode>
-__device__ int gemm_roles(const typename Mode::Args& args, const TmaPair& tm, uint8_t* tiles_smem,
+__device__ int gemm_roles(const typename Mode::Args& args, const TmaSet& tm, uint8_t* tiles_smem,
                           GemmSmem* S, int first, int tile_lo, int tile_hi,
-                          int* __restrict__ cursor) {
+                          int* __restrict__ cursor, const Timeline& tl) {
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = lane_id();
   uint8_t* sA = tiles_smem;
   uint8_t* sB = tiles_smem + STAGES * A_STAGE_BYTES;
-  int beyond = TASK_STOP;
 
   if (warp == 3) {
     // ---------------- scheduler: forwards tile ids, stops at the first non-tile id
@@ -36,18 +47,16 @@ __device__ int gemm_roles(const typename Mode::Args& args, const TmaPair& tm, ui
         S->ring[slot] = is_tile ? id - tile_lo : TASK_STOP;
         mbar_arrive(&S->rfull[slot]);
         if (!is_tile) {
-          beyond = id;
+          S->bcast = id;
           break;
         }
         id = atomicAdd(cursor, 1);
       }
-      S->bcast = beyond;
     }
   } else if (warp == 0) {
     // ---------------- TMA producer
     if (lane == 0) {
-      tma_prefetch_desc(&tm.a);
-      tma_prefetch_desc(&tm.b);
+      for (int i = 0; i < 4; ++i) tma_prefetch_desc(&tm.m[i]);
       uint32_t stage = 0, phase = 0;
       for (int it = 0;; ++it) {
         const int slot = it % RING;
@@ -57,6 +66,7 @@ __device__ int gemm_roles(const typename Mode::Args& args, const TmaPair& tm, ui
         if (t == TASK_STOP) break;
         const TileDesc td = Mode::tile(args, t);
         Mode::before_loads(args, td);
+        S->tstart[it & 7] = globaltimer();
         for (int kb = 0; kb < td.nkb; ++kb) {
           mbar_wait(&S->empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&S->full[stage], A_STAGE_BYTES + B_STAGE_BYTES);
@@ -74,7 +84,6 @@ __device__ int gemm_roles(const typename Mode::Args& args, const TmaPair& tm, ui
   } else if (warp == 1) {
     // ---------------- UMMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc(BM, BN, Mode::A_MN, Mode::B_MN);
       const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
       uint32_t stage = 0, phase = 0;
       for (int it = 0;; ++it) {
@@ -84,6 +93,8 @@ __device__ int gemm_roles(const typename Mode::Args& args, const TmaPair& tm, ui
         mbar_arrive(&S->rempty[slot]);
         if (t == TASK_STOP) break;
         const TileDesc td = Mode::tile(args, t);
+        const int amn = Mode::a_mn(td), bmn = Mode::b_mn(td);
+        const uint32_t idesc = make_idesc(BM, BN, amn, bmn);
         const uint32_t acc = it & 1;
         mbar_wait(&S->tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -95,10 +106,10 @@ __device__ int gemm_roles(const typename Mode::Args& args, const TmaPair& tm, ui
           const uint32_t bs = b0 + stage * B_STAGE_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = Mode::A_MN ? make_sdesc(as + k * 2048, 8192, 1024)
-                                           : make_sdesc(as + k * 32, 16, 1024);
-            const uint64_t bd = Mode::B_MN ? make_sdesc(bs + k * 2048, 8192, 1024)
-                                           : make_sdesc(bs + k * 32, 16, 1024);
+            const uint64_t ad = amn ? make_sdesc(as + k * 2048, 8192, 1024)
+                                    : make_sdesc(as + k * 32, 16, 1024);
+            const uint64_t bd = bmn ? make_sdesc(bs + k * 2048, 8192, 1024)
+                                    : make_sdesc(bs + k * 32, 16, 1024);
             umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
           }
           umma_commit(&S->empty[stage]);
@@ -130,6 +141,13 @@ __device__ int gemm_roles(const typename Mode::Args& args, const TmaPair& tm, ui
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&S->tempty[acc]);
+      if (Mode::HAS_TILE_DONE || tl.rec) {
+        epi_bar();  // all four epilogue warps finished this tile's stores
+        if (warp == 4 && lane == 0) {
+          if (Mode::HAS_TILE_DONE) Mode::tile_done(args, td);
+          timeline_push(tl, S->tstart[it & 7], globaltimer(), ROLE_COMP, t + tile_lo);
+        }
+      }
     }
   }
   __syncthreads();
@@ -194,6 +212,22 @@ __device__ __forceinline__ void store_zero_32(__nv_bfloat16* dst) {
   int4* d = reinterpret_cast<int4*>(dst);
 #pragma unroll
   for (int i = 0; i < 4; ++i) d[i] = make_int4(0, 0, 0, 0);
+}
+
+// 32 bf16 from global (4 x 16 B) into fp32.
+__device__ __forceinline__ void load_row_bf16_32(const __nv_bfloat16* src, float (&v)[32]) {
+  const int4* s = reinterpret_cast<const int4*>(src);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int4 w = s[i];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float2 f = __bfloat1622float2(h[k]);
+      v[8 * i + 2 * k] = f.x;
+      v[8 * i + 2 * k + 1] = f.y;
+    }
+  }
 }
 
 }  // namespace eplab_dev

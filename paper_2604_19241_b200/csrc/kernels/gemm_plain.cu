@@ -15,7 +15,10 @@
 namespace eplab_dev {
 
 struct ModeNT {
-  static constexpr int A_MN = 0, B_MN = 0;
+  static constexpr bool HAS_TILE_DONE = false;
+  __device__ static int a_mn(const TileDesc&) { return 0; }
+  __device__ static int b_mn(const TileDesc&) { return 0; }
+  template <class A> __device__ static void tile_done(const A&, const TileDesc&) {}
   struct Args {
     const TileDesc* tiles;
     __nv_bfloat16* C;
@@ -24,13 +27,13 @@ struct ModeNT {
   };
   __device__ static TileDesc tile(const Args& a, int t) { return a.tiles[t]; }
   __device__ static void before_loads(const Args&, const TileDesc&) {}
-  __device__ static void load_a(const Args&, const TmaPair& tm, uint64_t* bar, uint8_t* s,
+  __device__ static void load_a(const Args&, const TmaSet& tm, uint64_t* bar, uint8_t* s,
                                 const TileDesc& td, int kb) {
-    tma_load_2d(&tm.a, bar, s, kb * BK, td.m0);
+    tma_load_2d(&tm.m[0], bar, s, kb * BK, td.m0);
   }
-  __device__ static void load_b(const Args& a, const TmaPair& tm, uint64_t* bar, uint8_t* s,
+  __device__ static void load_b(const Args& a, const TmaSet& tm, uint64_t* bar, uint8_t* s,
                                 const TileDesc& td, int kb) {
-    tma_load_2d(&tm.b, bar, s, kb * BK, td.e * a.n_per_expert + td.n0);
+    tma_load_2d(&tm.m[1], bar, s, kb * BK, td.e * a.n_per_expert + td.n0);
   }
   __device__ static void epilogue(const Args& a, const TileDesc& td, uint32_t taddr, int r) {
     __nv_bfloat16* row = a.C + (size_t)(td.m0 + r) * a.ldc + td.n0;
@@ -45,7 +48,10 @@ struct ModeNT {
 };
 
 struct ModeTN {
-  static constexpr int A_MN = 1, B_MN = 1;
+  static constexpr bool HAS_TILE_DONE = false;
+  __device__ static int a_mn(const TileDesc&) { return 1; }
+  __device__ static int b_mn(const TileDesc&) { return 1; }
+  template <class A> __device__ static void tile_done(const A&, const TileDesc&) {}
   struct Args {
     const TileDesc* tiles;
     __nv_bfloat16* C;  // [E][rows_out][ldc]
@@ -54,17 +60,17 @@ struct ModeTN {
   };
   __device__ static TileDesc tile(const Args& a, int t) { return a.tiles[t]; }
   __device__ static void before_loads(const Args&, const TileDesc&) {}
-  __device__ static void load_a(const Args&, const TmaPair& tm, uint64_t* bar, uint8_t* s,
+  __device__ static void load_a(const Args&, const TmaSet& tm, uint64_t* bar, uint8_t* s,
                                 const TileDesc& td, int kb) {
 #pragma unroll
     for (int i = 0; i < BM / 64; ++i)
-      tma_load_2d(&tm.a, bar, s + i * 8192, td.m0 + 64 * i, td.kb0 + kb * BK);
+      tma_load_2d(&tm.m[0], bar, s + i * 8192, td.m0 + 64 * i, td.kb0 + kb * BK);
   }
-  __device__ static void load_b(const Args&, const TmaPair& tm, uint64_t* bar, uint8_t* s,
+  __device__ static void load_b(const Args&, const TmaSet& tm, uint64_t* bar, uint8_t* s,
                                 const TileDesc& td, int kb) {
 #pragma unroll
     for (int i = 0; i < BN / 64; ++i)
-      tma_load_2d(&tm.b, bar, s + i * 8192, td.n0 + 64 * i, td.kb0 + kb * BK);
+      tma_load_2d(&tm.m[1], bar, s + i * 8192, td.n0 + 64 * i, td.kb0 + kb * BK);
   }
   __device__ static void epilogue(const Args& a, const TileDesc& td, uint32_t taddr, int r) {
     __nv_bfloat16* row = a.C + td.e * a.expert_stride + (size_t)(td.m0 + r) * a.ldc + td.n0;
@@ -84,7 +90,7 @@ struct ModeTN {
 
 template <class Mode>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
-    plain_gemm_kernel(const __grid_constant__ TmaPair tm, const typename Mode::Args args,
+    plain_gemm_kernel(const __grid_constant__ TmaSet tm, const typename Mode::Args args,
                       int ntiles, int* cursor) {
   extern __shared__ uint8_t raw_smem[];
   uint8_t* base = smem_aligned(raw_smem);
@@ -94,7 +100,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __syncthreads();
   const int first = S->bcast;
   __syncthreads();
-  gemm_roles<Mode>(args, tm, base, S, first, 0, ntiles, cursor);
+  gemm_roles<Mode>(args, tm, base, S, first, 0, ntiles, cursor, Timeline{nullptr, nullptr, 0});
   gemm_teardown(S);
 }
 
@@ -114,7 +120,7 @@ int num_sms() {
 }
 
 template <class Mode>
-int launch_plain(const TmaPair& tm, const typename Mode::Args& args, const TileDesc* d_tiles,
+int launch_plain(const TmaSet& tm, const typename Mode::Args& args, const TileDesc* d_tiles,
                  int ntiles, int* d_cursor, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
@@ -157,9 +163,9 @@ int eplab_grouped_gemm_nt(const void* A, const void* B, void* C, int M_total, in
     int* d_cursor = (int*)((char*)d_workspace + sizeof(TileDesc) * tiles.size());
     cudaMemcpyAsync(d_tiles, tiles.data(), sizeof(TileDesc) * tiles.size(),
                     cudaMemcpyHostToDevice, st);
-    TmaPair tm;
-    tm.a = eplab_host::make_bf16_map(A, M_total, K, K, 64, BM);
-    tm.b = eplab_host::make_bf16_map(B, (uint64_t)n_experts * N, K, K, 64, BN);
+    TmaSet tm;
+    tm.m[0] = eplab_host::make_bf16_map(A, M_total, K, K, 64, BM);
+    tm.m[1] = tm.m[2] = tm.m[3] = eplab_host::make_bf16_map(B, (uint64_t)n_experts * N, K, K, 64, BN);
     ModeNT::Args args{d_tiles, (__nv_bfloat16*)C, N, N};
     return launch_plain<ModeNT>(tm, args, d_tiles, (int)tiles.size(), d_cursor, st);
   } catch (...) {
@@ -192,9 +198,9 @@ int eplab_grouped_gemm_tn(const void* A, const void* B, void* C, int M_total, in
     int* d_cursor = (int*)((char*)d_workspace + sizeof(TileDesc) * tiles.size());
     cudaMemcpyAsync(d_tiles, tiles.data(), sizeof(TileDesc) * tiles.size(),
                     cudaMemcpyHostToDevice, st);
-    TmaPair tm;
-    tm.a = eplab_host::make_bf16_map(A, M_total, NA, NA, 64, 64);
-    tm.b = eplab_host::make_bf16_map(B, M_total, NB, NB, 64, 64);
+    TmaSet tm;
+    tm.m[0] = eplab_host::make_bf16_map(A, M_total, NA, NA, 64, 64);
+    tm.m[1] = tm.m[2] = tm.m[3] = eplab_host::make_bf16_map(B, M_total, NB, NB, 64, 64);
     ModeTN::Args args{d_tiles, (__nv_bfloat16*)C, NB, (long long)NA * NB};
     return launch_plain<ModeTN>(tm, args, d_tiles, (int)tiles.size(), d_cursor, st);
   } catch (...) {

@@ -1,0 +1,695 @@
+// The EP-MoE MegaKernels, forward and backward, on the tcgen05 engine.
+//
+// Each kernel is persistent (one 256-thread CTA per SM). A CTA claims task ids from one
+// global cursor; the id space is linearised [pre | tiles | post] and claimed in that order,
+// so producers are always claimed before the consumers that wait on them (the deadlock
+// argument of types.cpp:55-67 / sim.cpp:547-551; Listing 1 :457-484).
+//
+//   fwd_dispatch_gemm  : [comm n_disp | relay n_relay | up-GEMM tiles (+SwiGLU)]
+//   fwd_gemm_combine   : [down-GEMM tiles (epilogue pushes replicas to the source) | reduce n_red]
+//   bwd_dispatch_gemm  : [comm n_disp (dY, gate grad) | relay | down-dgrad tiles (+SwiGLU bwd)
+//                         | down-wgrad tiles (transposed GroupGEMM)]
+//   bwd_gemm_combine   : [up-dgrad tiles (push dX replicas) | up-wgrad tiles | reduce n_red]
+//
+// Communication roles (the unified AllGather/AllToAll primitive):
+//   relay off (n_relay = 0, AllToAll style): a comm warp writes every (t, j) replica row
+//     straight into the destination slot and bumps the destination rowgroup counter with
+//     red.release.sys;
+//   relay on (AllGather style, sim.cpp:384-441): only the first (token, dst) item in
+//     priority order crosses NVLink; the sender writes the slot metadata of every replica
+//     and releases per-slot epoch flags; relay workers on the destination copy duplicates
+//     from the primary slot in HBM and count their rowgroups.
+// The comp tile waits for its rowgroup counter (ld.acquire.sys), fences the async proxy and
+// only then lets TMA read the rows: the token-granular scoreboard of Eq. 2.
+#include <cuda_runtime.h>
+
+#include "gemm_engine.cuh"
+#include "moe_common.cuh"
+
+namespace eplab_dev {
+
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ uint32_t* rg_counter(const SymPtrs& s, const Dims& d, int ph, int par,
+                                                int g) {
+  return s.rg_cnt + (size_t)(ph * 2 + par) * d.RG_cap + g;
+}
+__device__ __forceinline__ uint32_t* tok_counter(const SymPtrs& s, const Dims& d, int ph, int par,
+                                                 int t) {
+  return s.tok_cnt + (size_t)(ph * 2 + par) * d.T_max + t;
+}
+
+// Spin until *p >= target (acquire at system scope); the %globaltimer watchdog turns a
+// protocol bug into error 3 instead of a hung GPU.
+__device__ __forceinline__ void report_timeout(int* err, int site, uint32_t target, uint32_t seen,
+                                               int where) {
+  if (atomicCAS(err, 0, 3) == 0) {
+    err[1] = site;
+    err[2] = (int)target;
+    err[3] = (int)seen;
+    err[4] = where;
+  }
+}
+__device__ __forceinline__ void wait_geq_sys(const uint32_t* p, uint32_t target,
+                                             unsigned long long timeout, int* err, int site = 0,
+                                             int where = 0) {
+  if (ld_acquire_sys(p) >= target) return;
+  const unsigned long long t0 = globaltimer();
+  uint32_t v;
+  while ((v = ld_acquire_sys(p)) < target) {
+    if (globaltimer() - t0 > timeout) {
+      report_timeout(err, site, target, v, where);
+      return;
+    }
+  }
+}
+__device__ __forceinline__ void wait_eq_sys(const uint32_t* p, uint32_t want,
+                                            unsigned long long timeout, int* err, int site = 0,
+                                            int where = 0) {
+  if (ld_acquire_sys(p) == want) return;
+  const unsigned long long t0 = globaltimer();
+  uint32_t v;
+  while ((v = ld_acquire_sys(p)) != want) {
+    if (globaltimer() - t0 > timeout) {
+      report_timeout(err, site, want, v, where);
+      return;
+    }
+  }
+}
+
+// Local expert of a global 128-row block index g (binary search over mblock_pre).
+__device__ __forceinline__ int expert_of_block(const PlanDev& p, int epr, long long g) {
+  int lo = 0, hi = epr - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if ((long long)p.mblock_pre[mid] <= g)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+// NT tile t of a GEMM with `nb` column blocks over the receive layout, rasterised in groups
+// of G row blocks (column-major inside a group) so a group's A rows and the weight panel
+// stay resident in L2.
+constexpr int RASTER_G = 16;
+__device__ __forceinline__ void decode_nt(const Dims& d, const PlanDev& p, int t, int nb, int& e,
+                                          int& mblk, int& nblk) {
+  e = expert_of_block(p, d.epr, (long long)t / nb);
+  const int local = t - p.mblock_pre[e] * nb;
+  const int mbs = p.mblocks[e];
+  const int g = local / (RASTER_G * nb);
+  const int gsz = min(RASTER_G, mbs - g * RASTER_G);
+  const int r = local - g * RASTER_G * nb;
+  nblk = r / gsz;
+  mblk = g * RASTER_G + r % gsz;
+}
+
+__device__ __forceinline__ TileDesc nt_tile(const Dims& d, const PlanDev& p, int t, int nb,
+                                            int bn_cols, int nkb) {
+  int e, mb, nbk;
+  decode_nt(d, p, t, nb, e, mb, nbk);
+  TileDesc td;
+  const int ge = d.rank * d.epr + e;
+  td.e = e;
+  td.m0 = p.sb_all[ge] + mb * BM;
+  td.rows = min(BM, p.rt_all[ge] - mb * BM);
+  td.n0 = nbk * bn_cols;
+  td.kb0 = 0;
+  td.nkb = nkb;
+  td.pad0 = nbk;
+  td.pad1 = 0;
+  return td;
+}
+
+// Transposed (weight-gradient) tile t: output [NO][KO] per expert, BM x BN tiles row-major.
+__device__ __forceinline__ TileDesc tn_tile(const Dims& d, const PlanDev& p, int t, int NO, int KO) {
+  const int per_e = (NO / BM) * (KO / BN);
+  TileDesc td;
+  td.e = t / per_e;
+  const int l = t - td.e * per_e;
+  td.m0 = (l / (KO / BN)) * BM;
+  td.n0 = (l % (KO / BN)) * BN;
+  const int ge = d.rank * d.epr + td.e;
+  td.kb0 = p.sb_all[ge];
+  td.nkb = p.mblocks[td.e] * (BM / BK);
+  td.rows = BM;
+  td.pad0 = td.n0 / BN;
+  td.pad1 = 1;  // transposed tile
+  return td;
+}
+
+__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+
+// Even split of n into parts (sim.cpp:151-161).
+__device__ __forceinline__ void even_slice(long long n, int parts, int i, long long& lo,
+                                           long long& hi) {
+  const long long base = n / parts, rem = n % parts;
+  lo = i * base + (i < rem ? i : rem);
+  hi = lo + base + (i < rem ? 1 : 0);
+}
+
+// ------------------------------------------------------------------ comm role
+// One warp per send item, 16-byte vector copies. ph = 0 forward (x), 1 backward
+// (dY; the warp also folds the gate gradient <dY_t, o_{t,j}> of every item it visits).
+__device__ void comm_task(const MkArgs& a, int task, int ph) {
+  const Dims& d = a.d;
+  const int k = d.topk, H = d.H, me = d.rank;
+  const long long n = (long long)a.p.n_tok * k;
+  long long lo, hi;
+  even_slice(n, a.n_disp, task, lo, hi);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool relay_on = a.n_relay > 0;
+  const __nv_bfloat16* src_base = ph == 0 ? a.x : a.dy;
+  const uint32_t flagv = a.epoch * 2 + ph;
+  const int vecs = H / 8;
+  for (long long pi = lo + warp; pi < hi; pi += GEMM_THREADS / 32) {
+    const int i = a.p.sched[pi];
+    const int t = i / k, j = i - t * k;
+    const int e = a.p.topk_ids[i];
+    const int dst = e / d.epr, el = e - dst * d.epr;
+    const int slot = a.p.dst_slot[i];
+    bool primary = true;
+    if (relay_on)
+      for (int jj = 0; jj < k; ++jj) {
+        const int e2 = a.p.topk_ids[t * k + jj];
+        if (e2 / d.epr == dst && e2 - dst * d.epr < el) primary = false;
+      }
+    if (!primary && ph == 0) continue;
+    const int4* src = reinterpret_cast<const int4*>(src_base + (size_t)t * H);
+    const SymPtrs& P = a.peers.p[dst];
+    int4* dstrow = reinterpret_cast<int4*>(P.recv_x + (size_t)slot * H);
+    if (ph == 1) dstrow = reinterpret_cast<int4*>(P.recv_dy + (size_t)slot * H);
+    float gacc = 0.f;
+    const int4* orow = reinterpret_cast<const int4*>(a.peers.p[me].rep + (size_t)i * H);
+    for (int c = lane; c < vecs; c += 32) {
+      const int4 v = ld_nc_v4(src + c);
+      if (primary) dstrow[c] = v;
+      if (ph == 1) {
+        const int4 o = orow[c];
+        const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&v);
+        const __nv_bfloat162* ho = reinterpret_cast<const __nv_bfloat162*>(&o);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 fv = __bfloat1622float2(hv[q]), fo = __bfloat1622float2(ho[q]);
+          gacc = fmaf(fv.x, fo.x, gacc);
+          gacc = fmaf(fv.y, fo.y, gacc);
+        }
+      }
+    }
+    if (ph == 1) {
+#pragma unroll
+      for (int s = 16; s > 0; s >>= 1) gacc += __shfl_xor_sync(0xffffffffu, gacc, s);
+      if (lane == 0) a.dgate[i] = gacc;
+    }
+    if (!primary) continue;
+    if (ph == 0 && lane == 0) {
+      P.meta[slot] = SlotMeta{me, i, a.p.gate_w[i], -1};
+      if (relay_on)
+        for (int jj = 0; jj < k; ++jj) {
+          const int e2 = a.p.topk_ids[t * k + jj];
+          if (jj != j && e2 / d.epr == dst) {
+            const int s2 = a.p.dst_slot[t * k + jj];
+            P.meta[s2] = SlotMeta{me, t * k + jj, a.p.gate_w[t * k + jj], slot};
+          }
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_system();
+      if (relay_on) {
+        st_release_sys(P.slot_flag + slot, flagv);
+        for (int jj = 0; jj < k; ++jj) {
+          const int e2 = a.p.topk_ids[t * k + jj];
+          if (jj != j && e2 / d.epr == dst) st_release_sys(P.slot_flag + a.p.dst_slot[t * k + jj], flagv);
+        }
+      } else {
+        red_release_sys_add(rg_counter(P, d, ph, a.par, slot >> 7), 1u);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ relay role
+// Owns whole destination rowgroups (even split, sim.cpp:236-238); copies every duplicate
+// replica from its primary slot in HBM, then publishes the rowgroup count.
+__device__ void relay_task(const MkArgs& a, int task, int ph) {
+  const Dims& d = a.d;
+  const SymPtrs& me = a.peers.p[d.rank];
+  const int n_rg = a.p.scalars[1];
+  long long g0, g1;
+  even_slice(n_rg, a.n_relay, task, g0, g1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t flagv = a.epoch * 2 + ph;
+  __nv_bfloat16* recv = ph == 0 ? me.recv_x : me.recv_dy;
+  const int vecs = d.H / 8;
+  for (long long g = g0; g < g1; ++g) {
+    const int el = expert_of_block(a.p, d.epr, g);
+    const int ge = d.rank * d.epr + el;
+    const int rows = min(BM, a.p.rt_all[ge] - (int)(g - a.p.mblock_pre[el]) * BM);
+    for (int r = warp; r < rows; r += GEMM_THREADS / 32) {
+      const int s = (int)g * BM + r;
+      if (lane == 0) wait_eq_sys(me.slot_flag + s, flagv, a.timeout_ns, a.err, 10 + ph, s);
+      __syncwarp();
+      const int prim = me.meta[s].primary;
+      if (prim >= 0) {
+        const int4* src = reinterpret_cast<const int4*>(recv + (size_t)prim * d.H);
+        int4* dst = reinterpret_cast<int4*>(recv + (size_t)s * d.H);
+        for (int c = lane; c < vecs; c += 32) dst[c] = src[c];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      red_release_gpu_add(rg_counter(me, d, ph, a.par, (int)g), (uint32_t)rows);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ reduce role
+// Top-k completeness barrier, then the fixed k-ascending fold (
+// precision.cpp:31-37 order): forward y = bf16(fma-fold of w_j * o_j), backward
+// dx = bf16(sum_j dX_j), both in fp32.
+__device__ void reduce_task(const MkArgs& a, int task, int ph) {
+  const Dims& d = a.d;
+  const int k = d.topk, H = d.H;
+  const SymPtrs& me = a.peers.p[d.rank];
+  long long t0, t1;
+  even_slice(a.p.n_tok, a.n_red, task, t0, t1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t need = (uint32_t)(k * (H / BN));
+  const __nv_bfloat16* rep = ph == 0 ? me.rep : me.rep_dx;
+  __nv_bfloat16* out = ph == 0 ? a.y : a.dx;
+  for (long long t = t0 + warp; t < t1; t += GEMM_THREADS / 32) {
+    if (lane == 0)
+      wait_geq_sys(tok_counter(me, d, ph, a.par, (int)t), need, a.timeout_ns, a.err, 20 + ph, (int)t);
+    __syncwarp();
+    float w[16];
+    for (int j = 0; j < k; ++j) w[j] = ph == 0 ? a.p.gate_w[t * k + j] : 1.0f;
+    for (int c = lane * 8; c < H; c += 256) {
+      float acc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+      for (int j = 0; j < k; ++j) {
+        const int4 v = *reinterpret_cast<const int4*>(rep + ((size_t)t * k + j) * H + c);
+        const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 f = __bfloat1622float2(hv[q]);
+          if (ph == 0) {
+            acc[2 * q] = fmaf(w[j], f.x, acc[2 * q]);
+            acc[2 * q + 1] = fmaf(w[j], f.y, acc[2 * q + 1]);
+          } else {
+            acc[2 * q] = acc[2 * q] + f.x;
+            acc[2 * q + 1] = acc[2 * q + 1] + f.y;
+          }
+        }
+      }
+      int4 o;
+      o.x = (int)pack_bf16(acc[0], acc[1]);
+      o.y = (int)pack_bf16(acc[2], acc[3]);
+      o.z = (int)pack_bf16(acc[4], acc[5]);
+      o.w = (int)pack_bf16(acc[6], acc[7]);
+      *reinterpret_cast<int4*>(out + (size_t)t * H + c) = o;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ GEMM modes
+// tensor maps: m[0]/m[1] = A/B of the first tile type, m[2]/m[3] = A/B of the second.
+
+// Forward up projection: A = recv_x (K-major over H), B = W_up gate rows [f0,f0+128) and up
+// rows [F+f0, ..) (K-major). Epilogue: GU (bf16) and h = bf16(silu(g) * u) from the bf16 g, u.
+struct ModeUp {
+  using Args = MkArgs;
+  static constexpr bool HAS_TILE_DONE = false;
+  __device__ static int a_mn(const TileDesc&) { return 0; }
+  __device__ static int b_mn(const TileDesc&) { return 0; }
+  __device__ static TileDesc tile(const Args& a, int t) {
+    return nt_tile(a.d, a.p, t, a.d.F / 128, 128, a.d.H / BK);
+  }
+  __device__ static void before_loads(const Args& a, const TileDesc& td) {
+    const SymPtrs& me = a.peers.p[a.d.rank];
+    wait_geq_sys(rg_counter(me, a.d, 0, a.par, td.m0 >> 7), (uint32_t)td.rows, a.timeout_ns, a.err,
+                 30, td.m0 >> 7);
+    fence_proxy_async_global();
+  }
+  __device__ static void load_a(const Args&, const TmaSet& tm, uint64_t* bar, uint8_t* s,
+                                const TileDesc& td, int kb) {
+    tma_load_2d(&tm.m[0], bar, s, kb * BK, td.m0);
+  }
+  __device__ static void load_b(const Args& a, const TmaSet& tm, uint64_t* bar, uint8_t* s,
+                                const TileDesc& td, int kb) {
+    const int row = td.e * 2 * a.d.F + td.n0;
+    tma_load_2d(&tm.m[1], bar, s, kb * BK, row);
+    tma_load_2d(&tm.m[1], bar, s + 128 * 128, kb * BK, row + a.d.F);
+  }
+  __device__ static void epilogue(const Args& a, const TileDesc& td, uint32_t taddr, int r) {
+    const bool live = r < td.rows;  // tcgen05.ld is warp-collective: every lane loads
+    const size_t m = (size_t)td.m0 + r;
+    const int F = a.d.F;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      float g[32], u[32];
+      acc_chunk(taddr, c, g);
+      acc_chunk(taddr, 4 + c, u);
+      if (!live) continue;
+      __nv_bfloat16* gdst = a.gu + m * 2 * F + td.n0 + c * 32;
+      store_row_bf16_32(gdst, g);
+      store_row_bf16_32(gdst + F, u);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float gb = __bfloat162float(__float2bfloat16_rn(g[i]));
+        const float ub = __bfloat162float(__float2bfloat16_rn(u[i]));
+        g[i] = silu_f(gb) * ub;
+      }
+      store_row_bf16_32(a.hact + m * F + td.n0 + c * 32, g);
+    }
+  }
+  template <class A>
+  __device__ static void tile_done(const A&, const TileDesc&) {}
+};
+
+// Push the 128x256 output tile row by row into the source's replica slots (over NVLink when
+// the source is a peer) and count the column tile on the source token (combine scoreboard).
+__device__ __forceinline__ void push_rows(const MkArgs& a, const TileDesc& td, uint32_t taddr,
+                                          int r, int ph) {
+  const bool live = r < td.rows;
+  SlotMeta mt{0, 0, 0.f, 0};
+  if (live) mt = a.peers.p[a.d.rank].meta[td.m0 + r];
+  const SymPtrs& S = a.peers.p[live ? mt.src : 0];
+  __nv_bfloat16* dst = (ph == 0 ? S.rep : S.rep_dx) + (size_t)mt.rep * a.d.H + td.n0;
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    float v[32];
+    acc_chunk(taddr, c, v);
+    if (live) store_row_bf16_32(dst + c * 32, v);
+  }
+  if (live) red_release_sys_add(tok_counter(S, a.d, ph, a.par, mt.rep / a.d.topk), 1u);
+}
+
+// Forward down projection + combine push: A = hact (K-major over F), B = W_down (K-major).
+struct ModeDown {
+  using Args = MkArgs;
+  static constexpr bool HAS_TILE_DONE = false;
+  __device__ static int a_mn(const TileDesc&) { return 0; }
+  __device__ static int b_mn(const TileDesc&) { return 0; }
+  __device__ static TileDesc tile(const Args& a, int t) {
+    return nt_tile(a.d, a.p, t, a.d.H / BN, BN, a.d.F / BK);
+  }
+  __device__ static void before_loads(const Args&, const TileDesc&) {}
+  __device__ static void load_a(const Args&, const TmaSet& tm, uint64_t* bar, uint8_t* s,
+                                const TileDesc& td, int kb) {
+    tma_load_2d(&tm.m[0], bar, s, kb * BK, td.m0);
+  }
+  __device__ static void load_b(const Args& a, const TmaSet& tm, uint64_t* bar, uint8_t* s,
+                                const TileDesc& td, int kb) {
+    tma_load_2d(&tm.m[1], bar, s, kb * BK, td.e * a.d.H + td.n0);
+  }
+  __device__ static void epilogue(const Args& a, const TileDesc& td, uint32_t taddr, int r) {
+    push_rows(a, td, taddr, r, 0);
+  }
+  template <class A>
+  __device__ static void tile_done(const A&, const TileDesc&) {}
+};
+
+// Backward: down-dgrad tiles then down-wgrad tiles.
+//   dgrad : A = recv_dy (K-major over H), B = W_down[e] as [H rows = K][F cols] (MN-major).
+//           Epilogue: dh = w * acc; SwiGLU backward from the saved bf16 g, u; writes dGU and
+//           HW = bf16(w * h) (zeros on padding rows), then counts the (expert, f-block).
+//   wgrad : dW_down[e] = recv_dy_e^T . HW_e, A and B MN-major over the expert's rows, which
+//           are walked in ascending 64-row K-blocks (deterministic, no split-K).
+struct ModeDgradDown {
+  using Args = MkArgs;
+  static constexpr bool HAS_TILE_DONE = true;
+  __device__ static int n_dgrad(const Args& a) { return a.p.mblock_pre[a.d.epr] * (a.d.F / BN); }
+  __device__ static int a_mn(const TileDesc& td) { return td.pad1; }
+  __device__ static int b_mn(const TileDesc&) { return 1; }
+  __device__ static TileDesc tile(const Args& a, int t) {
+    const int nd = n_dgrad(a);
+    if (t < nd) return nt_tile(a.d, a.p, t, a.d.F / BN, BN, a.d.H / BK);
+    return tn_tile(a.d, a.p, t - nd, a.d.H, a.d.F);
+  }
+  __device__ static void before_loads(const Args& a, const TileDesc& td) {
+    if (!td.pad1) {
+      const SymPtrs& me = a.peers.p[a.d.rank];
+      wait_geq_sys(rg_counter(me, a.d, 1, a.par, td.m0 >> 7), (uint32_t)td.rows, a.timeout_ns,
+                   a.err, 31, td.m0 >> 7);
+    } else {
+      wait_geq_sys(a.wg_cnt + td.e * (a.d.F / BN) + td.pad0, (uint32_t)a.p.mblocks[td.e],
+                   a.timeout_ns, a.err, 32, td.e * 1000 + td.pad0);
+    }
+    fence_proxy_async_global();
+  }
+  __device__ static void load_a(const Args&, const TmaSet& tm, uint64_t* bar, uint8_t* s,
+                                const TileDesc& td, int kb) {
+    if (!td.pad1) {
+      tma_load_2d(&tm.m[0], bar, s, kb * BK, td.m0);
+    } else {
+#pragma unroll
+      for (int i = 0; i < BM / 64; ++i)
+        tma_load_2d(&tm.m[2], bar, s + i * 8192, td.m0 + 64 * i, td.kb0 + kb * BK);
+    }
+  }
+  __device__ static void load_b(const Args& a, const TmaSet& tm, uint64_t* bar, uint8_t* s,
+                                const TileDesc& td, int kb) {
+    if (!td.pad1) {
+#pragma unroll
+      for (int i = 0; i < BN / 64; ++i)
+        tma_load_2d(&tm.m[1], bar, s + i * 8192, td.n0 + 64 * i, td.e * a.d.H + kb * BK);
+    } else {
+#pragma unroll
+      for (int i = 0; i < BN / 64; ++i)
+        tma_load_2d(&tm.m[3], bar, s + i * 8192, td.n0 + 64 * i, td.kb0 + kb * BK);
+    }
+  }
+  __device__ static void epilogue(const Args& a, const TileDesc& td, uint32_t taddr, int r) {
+    const int F = a.d.F;
+    if (td.pad1) {  // weight gradient tile
+      __nv_bfloat16* row = a.dw_down + ((size_t)td.e * a.d.H + td.m0 + r) * F + td.n0;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        if (td.nkb > 0) {
+          acc_chunk(taddr, c, v);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        }
+        store_row_bf16_32(row + c * 32, v);
+      }
+      return;
+    }
+    const size_t m = (size_t)td.m0 + r;
+    const bool live = r < td.rows;
+    const float w = live ? a.peers.p[a.d.rank].meta[m].w : 0.f;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      float v[32];
+      acc_chunk(taddr, c, v);
+      const int f0 = td.n0 + c * 32;
+      __nv_bfloat16* dg = a.dgu + m * 2 * F + f0;
+      __nv_bfloat16* hwr = a.hw + m * F + f0;
+      if (!live) {
+        store_zero_32(dg);
+        store_zero_32(dg + F);
+        store_zero_32(hwr);
+        continue;
+      }
+      float g[32], u[32];
+      load_row_bf16_32(a.gu + m * 2 * F + f0, g);
+      load_row_bf16_32(a.gu + m * 2 * F + F + f0, u);
+      float du[32], hv[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float dh = w * v[i];
+        const float s = 1.0f / (1.0f + __expf(-g[i]));
+        const float si = g[i] * s;
+        const float ds = s * (1.0f + g[i] * (1.0f - s));
+        const float h = __bfloat162float(__float2bfloat16_rn(si * u[i]));
+        v[i] = dh * u[i] * ds;
+        du[i] = dh * si;
+        hv[i] = w * h;
+      }
+      store_row_bf16_32(dg, v);
+      store_row_bf16_32(dg + F, du);
+      store_row_bf16_32(hwr, hv);
+    }
+  }
+  __device__ static void tile_done(const Args& a, const TileDesc& td) {
+    if (td.pad1) return;
+    __threadfence();
+    red_release_gpu_add(a.wg_cnt + td.e * (a.d.F / BN) + td.pad0, 1u);
+  }
+};
+
+// Backward: up-dgrad tiles (push dX replicas to the source) then up-wgrad tiles.
+//   dgrad : A = dGU (K-major over 2F), B = W_up[e] as [2F rows = K][H cols] (MN-major).
+//   wgrad : dW_up[e] = dGU_e^T . recv_x_e (both MN-major over the expert's rows).
+struct ModeDgradUp {
+  using Args = MkArgs;
+  static constexpr bool HAS_TILE_DONE = false;
+  __device__ static int n_dgrad(const Args& a) { return a.p.mblock_pre[a.d.epr] * (a.d.H / BN); }
+  __device__ static int a_mn(const TileDesc& td) { return td.pad1; }
+  __device__ static int b_mn(const TileDesc&) { return 1; }
+  __device__ static TileDesc tile(const Args& a, int t) {
+    const int nd = n_dgrad(a);
+    if (t < nd) return nt_tile(a.d, a.p, t, a.d.H / BN, BN, 2 * a.d.F / BK);
+    return tn_tile(a.d, a.p, t - nd, 2 * a.d.F, a.d.H);
+  }
+  __device__ static void before_loads(const Args&, const TileDesc&) {}
+  __device__ static void load_a(const Args&, const TmaSet& tm, uint64_t* bar, uint8_t* s,
+                                const TileDesc& td, int kb) {
+    if (!td.pad1) {
+      tma_load_2d(&tm.m[0], bar, s, kb * BK, td.m0);
+    } else {
+#pragma unroll
+      for (int i = 0; i < BM / 64; ++i)
+        tma_load_2d(&tm.m[2], bar, s + i * 8192, td.m0 + 64 * i, td.kb0 + kb * BK);
+    }
+  }
+  __device__ static void load_b(const Args& a, const TmaSet& tm, uint64_t* bar, uint8_t* s,
+                                const TileDesc& td, int kb) {
+    if (!td.pad1) {
+#pragma unroll
+      for (int i = 0; i < BN / 64; ++i)
+        tma_load_2d(&tm.m[1], bar, s + i * 8192, td.n0 + 64 * i, td.e * 2 * a.d.F + kb * BK);
+    } else {
+#pragma unroll
+      for (int i = 0; i < BN / 64; ++i)
+        tma_load_2d(&tm.m[3], bar, s + i * 8192, td.n0 + 64 * i, td.kb0 + kb * BK);
+    }
+  }
+  __device__ static void epilogue(const Args& a, const TileDesc& td, uint32_t taddr, int r) {
+    if (!td.pad1) {
+      push_rows(a, td, taddr, r, 1);
+      return;
+    }
+    __nv_bfloat16* row = a.dw_up + ((size_t)td.e * 2 * a.d.F + td.m0 + r) * a.d.H + td.n0;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      float v[32];
+      if (td.nkb > 0) {
+        acc_chunk(taddr, c, v);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+      }
+      store_row_bf16_32(row + c * 32, v);
+    }
+  }
+  template <class A>
+  __device__ static void tile_done(const A&, const TileDesc&) {}
+};
+
+// ------------------------------------------------------------------ the MegaKernel
+// KIND 0: fwd dispatch+GEMM, 1: fwd GEMM+combine, 2: bwd dispatch+GEMM, 3: bwd GEMM+combine.
+template <int KIND, class Mode>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    megakernel(const __grid_constant__ TmaSet tm, const __grid_constant__ MkArgs a) {
+  extern __shared__ uint8_t raw_smem[];
+  uint8_t* base = smem_aligned(raw_smem);
+  GemmSmem* S = reinterpret_cast<GemmSmem*>(base + STAGES * (A_STAGE_BYTES + B_STAGE_BYTES));
+  const int ph = (KIND >= 2) ? 1 : 0;
+  const bool has_pre = (KIND == 0 || KIND == 2);
+  const bool has_post = (KIND == 1 || KIND == 3);
+
+  // Reset the other parity of this phase's counters (used one iteration ago, all their
+  // increments have landed) -- see DESIGN.md §Scoreboard.
+  if (blockIdx.x == 0) {
+    const SymPtrs& me = a.peers.p[a.d.rank];
+    if (has_pre)
+      for (int g = threadIdx.x; g < a.d.RG_cap; g += blockDim.x)
+        *rg_counter(me, a.d, ph, a.par ^ 1, g) = 0;
+    if (has_post)
+      for (int t = threadIdx.x; t < a.d.T_max; t += blockDim.x)
+        *tok_counter(me, a.d, ph, a.par ^ 1, t) = 0;
+  }
+  gemm_setup(S);
+
+  const int n_pre = has_pre ? a.n_disp + a.n_relay : 0;
+  int n_tiles = 0;
+  if (KIND == 0) n_tiles = a.p.mblock_pre[a.d.epr] * (a.d.F / 128);
+  if (KIND == 1) n_tiles = a.p.mblock_pre[a.d.epr] * (a.d.H / BN);
+  if (KIND == 2)
+    n_tiles = a.p.mblock_pre[a.d.epr] * (a.d.F / BN) + a.d.epr * (a.d.H / BM) * (a.d.F / BN);
+  if (KIND == 3)
+    n_tiles = a.p.mblock_pre[a.d.epr] * (a.d.H / BN) + a.d.epr * (2 * a.d.F / BM) * (a.d.H / BN);
+  const int n_post = has_post ? a.n_red : 0;
+  const int total = n_pre + n_tiles + n_post;
+
+  if (threadIdx.x == 0) S->bcast = atomicAdd(a.cursor, 1);
+  __syncthreads();
+  int id = S->bcast;
+  __syncthreads();
+  // pre-tasks (comm / relay): the whole CTA
+  while (id < n_pre) {
+    const unsigned long long t0 = globaltimer();
+    if (id < a.n_disp)
+      comm_task(a, id, ph);
+    else
+      relay_task(a, id - a.n_disp, ph);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      timeline_push(a.tl, t0, globaltimer(), id < a.n_disp ? ROLE_COMM : ROLE_RELAY, id);
+      S->bcast = atomicAdd(a.cursor, 1);
+    }
+    __syncthreads();
+    id = S->bcast;
+    __syncthreads();
+  }
+  // compute tiles: warp-specialised engine
+  if (id < n_pre + n_tiles)
+    id = gemm_roles<Mode>(a, tm, base, S, id, n_pre, n_pre + n_tiles, a.cursor, a.tl);
+  // post-tasks (reduce): the whole CTA
+  while (id < total) {
+    const unsigned long long t0 = globaltimer();
+    reduce_task(a, id - n_pre - n_tiles, ph);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      timeline_push(a.tl, t0, globaltimer(), ROLE_REDUCE, id);
+      S->bcast = atomicAdd(a.cursor, 1);
+    }
+    __syncthreads();
+    id = S->bcast;
+    __syncthreads();
+  }
+  gemm_teardown(S);
+}
+
+}  // namespace eplab_dev
+
+// ------------------------------------------------------------------ host launchers
+namespace eplab_launch {
+using namespace eplab_dev;
+
+template <int KIND, class Mode>
+static int launch_mk(const TmaSet& tm, const MkArgs& a, int grid, cudaStream_t st) {
+  static bool attr = false;
+  auto fn = megakernel<KIND, Mode>;
+  if (!attr) {
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)GEMM_SMEM_BYTES) != cudaSuccess)
+      return 1;
+    attr = true;
+  }
+  cudaMemsetAsync(a.cursor, 0, sizeof(int), st);
+  fn<<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, st>>>(tm, a);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int launch_fwd_dispatch(const TmaSet& tm, const MkArgs& a, int grid, cudaStream_t st) {
+  return launch_mk<0, ModeUp>(tm, a, grid, st);
+}
+int launch_fwd_combine(const TmaSet& tm, const MkArgs& a, int grid, cudaStream_t st) {
+  return launch_mk<1, ModeDown>(tm, a, grid, st);
+}
+int launch_bwd_dispatch(const TmaSet& tm, const MkArgs& a, int grid, cudaStream_t st) {
+  return launch_mk<2, ModeDgradDown>(tm, a, grid, st);
+}
+int launch_bwd_combine(const TmaSet& tm, const MkArgs& a, int grid, cudaStream_t st) {
+  return launch_mk<3, ModeDgradUp>(tm, a, grid, st);
+}
+
+}  // namespace eplab_launch

@@ -1,0 +1,284 @@
+"""Python mirror of the EP-MoE data path (drop-in for the reference's dispatch / group_gemm /
+combine entry points), over the C-ABI of libeplab_b200.so.
+
+PyTorch supplies device memory, streams and torch.distributed bootstrap only; every
+computation runs in the library's sm_100a kernels. There is no CPU fallback: without the
+library or a CUDA device every call raises.
+"""
+import ctypes as C
+
+import torch
+
+from . import _lib
+
+_P = C.c_void_p
+_I = C.c_int
+
+
+class InitArgs(C.Structure):
+    _fields_ = [("rank", _I), ("world", _I), ("device", _I), ("max_tokens", _I), ("hidden", _I),
+                ("ffn", _I), ("n_experts", _I), ("topk", _I), ("max_recv_rows", C.c_longlong),
+                ("timeout_s", C.c_double)]
+
+
+class TuneConfig(C.Structure):
+    """Reference TuneConfig (types.hpp:45-53)."""
+    _fields_ = [("n_disp", _I), ("n_relay", _I), ("n_comb", _I), ("n_red", _I), ("w", _I)]
+
+    def __repr__(self):
+        return f"TuneConfig({self.n_disp},{self.n_relay},{self.n_comb},{self.n_red},{self.w})"
+
+
+class EplabError(RuntimeError):
+    """Raised on a non-zero C-ABI return: .code is 1 (internal), 2 (validation, the reference's
+    ValidationError) or 3 (deadlock / watchdog, the reference's DeadlockError)."""
+
+    def __init__(self, code, msg):
+        super().__init__(f"[eplab rc={code}] {msg}")
+        self.code = code
+
+
+_SIGS = {
+    "eplab_init": [C.POINTER(InitArgs), C.POINTER(_P)],
+    "eplab_destroy": [_P],
+    "eplab_ipc_handle": [_P, _P],
+    "eplab_connect_ipc": [_P, _P],
+    "eplab_connect_local": [C.POINTER(_P), _I],
+    "eplab_set_tune_config": [_P, C.POINTER(TuneConfig)],
+    "eplab_get_tune_config": [_P, C.POINTER(TuneConfig)],
+    "eplab_set_sm_budget": [_P, _I],
+    "eplab_plan": [_P, _P, _P, _I, _P],
+    "eplab_dispatch_group_gemm": [_P, _P, _P, _P],
+    "eplab_group_gemm_combine": [_P, _P, _P, _P],
+    "eplab_dispatch_group_gemm_bwd": [_P, _P, _P, _P, _P, _P],
+    "eplab_group_gemm_combine_bwd": [_P, _P, _P, _P, _P],
+    "eplab_moe_fwd": [_P, _P, _P, _I, _P, _P, _P, _P, _P],
+    "eplab_moe_bwd": [_P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "eplab_moe_step_host": [_P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "eplab_check": [_P, _P],
+    "eplab_export_token_map": [_P, _P, _P, _P, _P, _P],
+    "eplab_export_schedule": [_P, _P, _P],
+    "eplab_export_layout": [_P, _P, _P],
+    "eplab_timeline_enable": [_P, _I],
+    "eplab_timeline_export": [_P, C.c_char_p, C.POINTER(C.c_double)],
+}
+
+
+def lib():
+    L = _lib.lib()
+    if not getattr(L, "_eplab_sigs", False):
+        for name, args in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = _I
+        L.eplab_buffer.argtypes = [_P, C.c_char_p]
+        L.eplab_buffer.restype = _P
+        L.eplab_last_error.argtypes = [C.c_char_p, C.c_size_t]
+        L.eplab_last_error.restype = C.c_size_t
+        L._eplab_sigs = True
+    return L
+
+
+def _check(rc):
+    if rc:
+        buf = C.create_string_buffer(1024)
+        lib().eplab_last_error(buf, 1024)
+        raise EplabError(rc, buf.value.decode(errors="replace"))
+
+
+def _ptr(t):
+    return None if t is None else _P(t.data_ptr())
+
+
+def _stream(stream):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return _P(s.cuda_stream)
+
+
+class EpMoE:
+    """One rank of the expert-parallel MoE layer (experts sharded contiguously: rank = e // epr).
+
+    Tensors: x, dy [n_tok, H] bf16; topk_ids [n_tok, k] int32; gate_w [n_tok, k] fp32;
+    w_up [E_loc, 2F, H] bf16 (gate rows [0,F), up rows [F,2F)); w_down [E_loc, H, F] bf16.
+    """
+
+    def __init__(self, hidden, ffn, n_experts, topk, max_tokens, rank=0, world=1, device=None,
+                 max_recv_rows=0, timeout_s=10.0):
+        if not torch.cuda.is_available():
+            raise RuntimeError("EpMoE needs a CUDA (sm_100a) device; there is no CPU path")
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.device = dev
+        self.H, self.F, self.E, self.k, self.T_max = hidden, ffn, n_experts, topk, max_tokens
+        self.rank, self.world, self.epr = rank, world, n_experts // world
+        a = InitArgs(rank, world, dev.index, max_tokens, hidden, ffn, n_experts, topk, max_recv_rows,
+                     timeout_s)
+        h = _P()
+        with torch.cuda.device(dev):
+            _check(lib().eplab_init(C.byref(a), C.byref(h)))
+        self.h = h
+        self._ids = self._gw = None
+
+    def close(self):
+        if self.h:
+            lib().eplab_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ wiring
+    @staticmethod
+    def connect_local(ranks):
+        arr = (_P * len(ranks))(*[r.h for r in ranks])
+        _check(lib().eplab_connect_local(arr, len(ranks)))
+
+    def ipc_handle(self):
+        buf = (C.c_char * 64)()
+        _check(lib().eplab_ipc_handle(self.h, buf))
+        return bytes(buf)
+
+    def connect_ipc(self, handles):
+        blob = b"".join(handles)
+        _check(lib().eplab_connect_ipc(self.h, C.c_char_p(blob)))
+
+    def connect_distributed(self, group=None):
+        """Bootstrap over torch.distributed (NCCL or gloo): all-gather the IPC handles."""
+        import torch.distributed as dist
+        hs = [None] * self.world
+        dist.all_gather_object(hs, self.ipc_handle(), group=group)
+        self.connect_ipc(hs)
+
+    def set_tune_config(self, cfg):
+        if isinstance(cfg, (tuple, list)):
+            cfg = TuneConfig(*cfg)
+        _check(lib().eplab_set_tune_config(self.h, C.byref(cfg)))
+
+    def tune_config(self):
+        c = TuneConfig()
+        lib().eplab_get_tune_config(self.h, C.byref(c))
+        return c
+
+    def set_sm_budget(self, n_sm):
+        _check(lib().eplab_set_sm_budget(self.h, n_sm))
+
+    # ------------------------------------------------------------------ data path
+    def plan(self, topk_ids, gate_w, stream=None):
+        assert topk_ids.dtype == torch.int32 and gate_w.dtype == torch.float32
+        self._ids, self._gw = topk_ids.contiguous(), gate_w.contiguous()
+        _check(lib().eplab_plan(self.h, _ptr(self._ids), _ptr(self._gw), self._ids.shape[0],
+                                _stream(stream)))
+
+    def dispatch_group_gemm(self, x, w_up, stream=None):
+        _check(lib().eplab_dispatch_group_gemm(self.h, _ptr(x), _ptr(w_up), _stream(stream)))
+
+    def group_gemm_combine(self, w_down, y=None, stream=None):
+        n = self._ids.shape[0]
+        if y is None:
+            y = torch.empty(n, self.H, dtype=torch.bfloat16, device=self.device)
+        _check(lib().eplab_group_gemm_combine(self.h, _ptr(w_down), _ptr(y), _stream(stream)))
+        return y
+
+    def forward(self, x, topk_ids, gate_w, w_up, w_down, stream=None):
+        self.plan(topk_ids, gate_w, stream)
+        self.dispatch_group_gemm(x, w_up, stream)
+        return self.group_gemm_combine(w_down, stream=stream)
+
+    def backward(self, dy, w_up, w_down, stream=None, out=None):
+        n = self._ids.shape[0]
+        dev = self.device
+        if out is None:
+            out = dict(dx=torch.empty(n, self.H, dtype=torch.bfloat16, device=dev),
+                       dw_up=torch.empty_like(w_up), dw_down=torch.empty_like(w_down),
+                       dgate=torch.empty(n, self.k, dtype=torch.float32, device=dev))
+        _check(lib().eplab_dispatch_group_gemm_bwd(self.h, _ptr(dy), _ptr(w_down), _ptr(out["dw_down"]),
+                                                   _ptr(out["dgate"]), _stream(stream)))
+        _check(lib().eplab_group_gemm_combine_bwd(self.h, _ptr(w_up), _ptr(out["dx"]), _ptr(out["dw_up"]),
+                                                  _stream(stream)))
+        return out
+
+    def step_host(self, ids_h, gw_h, x_h, dy_h, w_up, w_down, y_h, dx_h, dgate_h, dw_up, dw_down,
+                  stream=None):
+        """fwd+bwd through the C-ABI with HOST routing/activations (copies inside the call)."""
+        _check(lib().eplab_moe_step_host(self.h, _ptr(ids_h), _ptr(gw_h), ids_h.shape[0], _ptr(x_h),
+                                         _ptr(dy_h), _ptr(w_up), _ptr(w_down), _ptr(y_h), _ptr(dx_h),
+                                         _ptr(dgate_h), _ptr(dw_up), _ptr(dw_down), _stream(stream)))
+
+    def check(self, stream=None):
+        _check(lib().eplab_check(self.h, _stream(stream)))
+
+    # ------------------------------------------------------------------ exports
+    def export_token_map(self):
+        import numpy as np
+        n = self._ids.shape[0] * self.k
+        tr = np.zeros(n, np.int32)
+        le = np.zeros(n, np.int32)
+        off = np.zeros(n, np.int64)
+        rt = np.zeros(self.world * self.epr, np.int64)
+        sb = np.zeros(self.world * self.epr, np.int64)
+        _check(lib().eplab_export_token_map(self.h, tr.ctypes.data, le.ctypes.data, off.ctypes.data,
+                                            rt.ctypes.data, sb.ctypes.data))
+        return tr, le, off, rt, sb
+
+    def export_schedule(self):
+        import numpy as np
+        n = self._ids.shape[0] * self.k
+        tok = np.zeros(n, np.int64)
+        slot = np.zeros(n, np.int32)
+        _check(lib().eplab_export_schedule(self.h, tok.ctypes.data, slot.ctypes.data))
+        return tok, slot
+
+    def export_layout(self):
+        import numpy as np
+        sb = np.zeros(self.epr, np.int32)
+        rows = np.zeros(self.epr, np.int32)
+        _check(lib().eplab_export_layout(self.h, sb.ctypes.data, rows.ctypes.data))
+        return sb, rows
+
+    def buffer(self, name, rows, cols):
+        """bf16 view of an internal device buffer (tests / profiling)."""
+        p = lib().eplab_buffer(self.h, name.encode())
+        if not p:
+            raise KeyError(name)
+        return _DeviceView(p, rows, cols, self.device).tensor()
+
+    def timeline_enable(self, cap=1 << 20):
+        _check(lib().eplab_timeline_enable(self.h, cap))
+
+    def timeline_export(self, path=""):
+        f = C.c_double()
+        _check(lib().eplab_timeline_export(self.h, path.encode(), C.byref(f)))
+        return f.value
+
+
+class _DeviceView:
+    """Wraps a raw device pointer as a torch tensor via __cuda_array_interface__."""
+
+    def __init__(self, ptr, rows, cols, device):
+        self.__cuda_array_interface__ = {"shape": (rows, cols), "typestr": "<i2", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+        self.device = device
+
+    def tensor(self):
+        with torch.cuda.device(self.device):
+            return torch.as_tensor(self, device=self.device).view(torch.bfloat16)
+
+
+class EpMoEFunction(torch.autograd.Function):
+    """Autograd wrapper: y = MoE(x; routing, gate weights, W_up, W_down). Gradients flow to x,
+    gate_w (the router output), w_up and w_down; routing ids are integer inputs."""
+
+    @staticmethod
+    def forward(ctx, layer, x, topk_ids, gate_w, w_up, w_down):
+        y = layer.forward(x, topk_ids, gate_w, w_up, w_down)
+        ctx.layer = layer
+        ctx.save_for_backward(w_up, w_down)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        w_up, w_down = ctx.saved_tensors
+        g = ctx.layer.backward(dy.contiguous(), w_up, w_down)
+        return None, g["dx"], None, g["dgate"], g["dw_up"], g["dw_down"]

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <sstream>
@@ -62,6 +63,7 @@ struct eplab_ctx {
   // fixed tensor maps
   CUtensorMap tm_recv_x_k{}, tm_recv_x_mn{}, tm_hact_k{}, tm_recv_dy_k{}, tm_recv_dy_mn{},
       tm_hw_mn{}, tm_dgu_k{}, tm_dgu_mn{};
+  CUtensorMap st_gu{}, st_hact{}, st_dgu{}, st_hw{};  // epilogue store maps
   // iteration state
   uint32_t epoch = 0;
   bool planned = false;
@@ -126,6 +128,7 @@ MkArgs base_args(eplab_ctx* c) {
   a.n_red = std::max(1, c->cfg.n_red);
   a.timeout_ns = c->timeout_ns;
   a.tl = Timeline{c->tl_rec, c->tl_count, c->tl_cap};
+  a.dbg = getenv("EPLAB_DBG") ? atoi(getenv("EPLAB_DBG")) : 0;
   return a;
 }
 
@@ -253,6 +256,10 @@ int eplab_init(const eplab_init_args* args, eplab_ctx** out) {
     c->tm_hw_mn = make_bf16_map(c->hw, M, d.F, d.F, 64, 64);
     c->tm_dgu_k = make_bf16_map(c->dgu, M, 2 * d.F, 2 * d.F, 64, 128);
     c->tm_dgu_mn = make_bf16_map(c->dgu, M, 2 * d.F, 2 * d.F, 64, 64);
+    c->st_gu = eplab_host::make_store_map(c->gu, M, 2 * d.F);
+    c->st_hact = eplab_host::make_store_map(c->hact, M, d.F);
+    c->st_dgu = eplab_host::make_store_map(c->dgu, M, 2 * d.F);
+    c->st_hw = eplab_host::make_store_map(c->hw, M, d.F);
     CK(cudaDeviceSynchronize());
     *out = c;
   });
@@ -386,6 +393,9 @@ int eplab_dispatch_group_gemm(eplab_ctx* c, const void* x, const void* w_up, voi
     tm.m[1] = eplab_host::make_bf16_map(w_up, (uint64_t)c->d.epr * 2 * c->d.F, c->d.H, c->d.H, 64, 128);
     tm.m[2] = tm.m[0];
     tm.m[3] = tm.m[1];
+    tm.m[4] = c->st_gu;
+    tm.m[5] = c->st_hact;
+    tm.m[6] = tm.m[7] = c->st_gu;
     if (eplab_launch::launch_fwd_dispatch(tm, a, c->num_sms, (cudaStream_t)stream))
       throw Fail{EPLAB_ERR_INTERNAL, std::string("dispatch launch: ") +
                                          cudaGetErrorString(cudaGetLastError())};
@@ -404,6 +414,7 @@ int eplab_group_gemm_combine(eplab_ctx* c, const void* w_down, void* y, void* st
     tm.m[1] = eplab_host::make_bf16_map(w_down, (uint64_t)c->d.epr * c->d.H, c->d.F, c->d.F, 64, 256);
     tm.m[2] = tm.m[0];
     tm.m[3] = tm.m[1];
+    tm.m[4] = tm.m[5] = tm.m[6] = tm.m[7] = c->st_gu;
     if (eplab_launch::launch_fwd_combine(tm, a, c->num_sms, (cudaStream_t)stream))
       throw Fail{EPLAB_ERR_INTERNAL, std::string("combine launch: ") +
                                          cudaGetErrorString(cudaGetLastError())};
@@ -427,6 +438,10 @@ int eplab_dispatch_group_gemm_bwd(eplab_ctx* c, const void* dy, const void* w_do
     tm.m[1] = eplab_host::make_bf16_map(w_down, (uint64_t)c->d.epr * c->d.H, c->d.F, c->d.F, 64, 64);
     tm.m[2] = c->tm_recv_dy_mn;
     tm.m[3] = c->tm_hw_mn;
+    tm.m[4] = c->st_dgu;
+    tm.m[5] = c->st_hw;
+    tm.m[6] = eplab_host::make_store_map(dw_down, (uint64_t)c->d.epr * c->d.H, c->d.F);
+    tm.m[7] = tm.m[6];
     if (eplab_launch::launch_bwd_dispatch(tm, a, c->num_sms, st))
       throw Fail{EPLAB_ERR_INTERNAL, std::string("bwd dispatch launch: ") +
                                          cudaGetErrorString(cudaGetLastError())};
@@ -447,6 +462,9 @@ int eplab_group_gemm_combine_bwd(eplab_ctx* c, const void* w_up, void* dx, void*
     tm.m[1] = eplab_host::make_bf16_map(w_up, (uint64_t)c->d.epr * 2 * c->d.F, c->d.H, c->d.H, 64, 64);
     tm.m[2] = c->tm_dgu_mn;
     tm.m[3] = c->tm_recv_x_mn;
+    tm.m[4] = tm.m[5] = c->st_dgu;
+    tm.m[6] = eplab_host::make_store_map(dw_up, (uint64_t)c->d.epr * 2 * c->d.F, c->d.H);
+    tm.m[7] = tm.m[6];
     if (eplab_launch::launch_bwd_combine(tm, a, c->num_sms, (cudaStream_t)stream))
       throw Fail{EPLAB_ERR_INTERNAL, std::string("bwd combine launch: ") +
                                          cudaGetErrorString(cudaGetLastError())};

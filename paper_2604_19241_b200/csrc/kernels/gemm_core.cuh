@@ -27,7 +27,7 @@ constexpr int BN = 256;
 constexpr int BK = 64;
 constexpr int STAGES = 4;
 constexpr int ACC_STAGES = 2;
-constexpr int RING = 2;
+constexpr int RING = 4;
 constexpr int GEMM_THREADS = 256;
 constexpr uint32_t A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 constexpr uint32_t B_STAGE_BYTES = BN * BK * 2;  // 32 KB
@@ -54,13 +54,20 @@ struct GemmSmem {
   uint64_t rfull[RING];
   uint64_t rempty[RING];
   unsigned long long tstart[8];
+  TileDesc ring_td[RING];
   int ring[RING];
   uint32_t tmem_base;
   int bcast;
 };
 
+// Epilogue staging: per epilogue warp three 32x32 bf16 tiles (64 B rows, 64B-swizzled) that the
+// warp's elected lane writes out with TMA bulk-tensor stores.
+constexpr uint32_t EPI_TILE_BYTES = 32 * 64;
+constexpr uint32_t EPI_WARP_BYTES = 3 * EPI_TILE_BYTES;
+constexpr uint32_t EPI_BYTES = 4 * EPI_WARP_BYTES;
+constexpr uint32_t TILES_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES);
 constexpr uint32_t GEMM_SMEM_BYTES =
-    1024 /*align slack*/ + STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + sizeof(GemmSmem) + 64;
+    1024 /*align slack*/ + TILES_BYTES + EPI_BYTES + sizeof(GemmSmem) + 64;
 
 __device__ __forceinline__ uint8_t* smem_aligned(uint8_t* raw) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));

@@ -37,14 +37,21 @@ __device__ int gemm_roles(const typename Mode::Args& args, const TmaSet& tm, uin
   uint8_t* sB = tiles_smem + STAGES * A_STAGE_BYTES;
 
   if (warp == 3) {
-    // ---------------- scheduler: forwards tile ids, stops at the first non-tile id
+    // ---------------- scheduler: claims tile ids, decodes them and resolves their scoreboard
+    // dependencies (Mode::before_loads) ahead of the producer; stops at the first non-tile id
     if (lane == 0) {
       int id = first;
       for (int it = 0;; ++it) {
         const int slot = it % RING;
-        mbar_wait(&S->rempty[slot], ((it / RING) & 1) ^ 1);
         const bool is_tile = id >= tile_lo && id < tile_hi;
+        TileDesc td{};
+        if (is_tile) {
+          td = Mode::tile(args, id - tile_lo);
+          Mode::before_loads(args, td);
+        }
+        mbar_wait(&S->rempty[slot], ((it / RING) & 1) ^ 1);
         S->ring[slot] = is_tile ? id - tile_lo : TASK_STOP;
+        S->ring_td[slot] = td;
         mbar_arrive(&S->rfull[slot]);
         if (!is_tile) {
           S->bcast = id;
@@ -56,16 +63,16 @@ __device__ int gemm_roles(const typename Mode::Args& args, const TmaSet& tm, uin
   } else if (warp == 0) {
     // ---------------- TMA producer
     if (lane == 0) {
-      for (int i = 0; i < 4; ++i) tma_prefetch_desc(&tm.m[i]);
+      for (int i = 0; i < 8; ++i) tma_prefetch_desc(&tm.m[i]);
       uint32_t stage = 0, phase = 0;
       for (int it = 0;; ++it) {
         const int slot = it % RING;
         mbar_wait(&S->rfull[slot], (it / RING) & 1);
         const int t = S->ring[slot];
+        const TileDesc td = S->ring_td[slot];
         mbar_arrive(&S->rempty[slot]);
         if (t == TASK_STOP) break;
-        const TileDesc td = Mode::tile(args, t);
-        Mode::before_loads(args, td);
+        fence_proxy_async_global();  // scoreboard acquired by the scheduler -> async-proxy reads
         S->tstart[it & 7] = globaltimer();
         for (int kb = 0; kb < td.nkb; ++kb) {
           mbar_wait(&S->empty[stage], phase ^ 1);
@@ -90,9 +97,9 @@ __device__ int gemm_roles(const typename Mode::Args& args, const TmaSet& tm, uin
         const int slot = it % RING;
         mbar_wait(&S->rfull[slot], (it / RING) & 1);
         const int t = S->ring[slot];
+        const TileDesc td = S->ring_td[slot];
         mbar_arrive(&S->rempty[slot]);
         if (t == TASK_STOP) break;
-        const TileDesc td = Mode::tile(args, t);
         const int amn = Mode::a_mn(td), bmn = Mode::b_mn(td);
         const uint32_t idesc = make_idesc(BM, BN, amn, bmn);
         const uint32_t acc = it & 1;
@@ -129,15 +136,19 @@ __device__ int gemm_roles(const typename Mode::Args& args, const TmaSet& tm, uin
       const int slot = it % RING;
       mbar_wait(&S->rfull[slot], (it / RING) & 1);
       const int t = S->ring[slot];
+      const TileDesc td = S->ring_td[slot];
       __syncwarp();
       if (lane == 0) mbar_arrive(&S->rempty[slot]);
-      if (t == TASK_STOP) break;
-      const TileDesc td = Mode::tile(args, t);
+      if (t == TASK_STOP) {
+        if (lane == 0) tma_store_wait<0>();  // outstanding epilogue stores before teardown
+        break;
+      }
+      Mode::epilogue_prefetch(args, td, r);
       const uint32_t acc = it & 1;
       mbar_wait(&S->tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t taddr = S->tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
-      Mode::epilogue(args, td, taddr, r);
+      Mode::epilogue(args, tm, td, taddr, r, tiles_smem + TILES_BYTES + q * EPI_WARP_BYTES);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&S->tempty[acc]);
@@ -228,6 +239,36 @@ __device__ __forceinline__ void load_row_bf16_32(const __nv_bfloat16* src, float
       v[8 * i + 2 * k + 1] = f.y;
     }
   }
+}
+
+
+// ---------------------------------------------------------------- staged TMA-store epilogue
+// Row r (0..31) of a warp's 32x32 bf16 staging tile, 64B-swizzled (16 B chunk c of row r lives at
+// chunk c ^ ((r >> 1) & 3)) so the 32 lanes' 16 B stores hit distinct bank groups.
+__device__ __forceinline__ void stage_row(uint8_t* buf, int r, const float (&v)[32]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    int4 w;
+    w.x = (int)pack_bf16(v[8 * c + 0], v[8 * c + 1]);
+    w.y = (int)pack_bf16(v[8 * c + 2], v[8 * c + 3]);
+    w.z = (int)pack_bf16(v[8 * c + 4], v[8 * c + 5]);
+    w.w = (int)pack_bf16(v[8 * c + 6], v[8 * c + 7]);
+    *reinterpret_cast<int4*>(buf + r * 64 + ((c ^ ((r >> 1) & 3)) << 4)) = w;
+  }
+}
+__device__ __forceinline__ void stage_zero_row(uint8_t* buf, int r) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) *reinterpret_cast<int4*>(buf + r * 64 + (c << 4)) = make_int4(0, 0, 0, 0);
+}
+// Before refilling the warp's staging tiles: the previous TMA stores must have read them.
+__device__ __forceinline__ void stage_acquire(uint32_t lane) {
+  if (lane == 0) tma_store_wait_read<0>();
+  __syncwarp();
+}
+// After filling: make generic-proxy smem writes visible to the TMA engine.
+__device__ __forceinline__ void stage_release() {
+  fence_proxy_async();
+  __syncwarp();
 }
 
 }  // namespace eplab_dev

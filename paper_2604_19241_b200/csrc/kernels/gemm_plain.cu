@@ -27,6 +27,7 @@ struct ModeNT {
   };
   __device__ static TileDesc tile(const Args& a, int t) { return a.tiles[t]; }
   __device__ static void before_loads(const Args&, const TileDesc&) {}
+  __device__ static void epilogue_prefetch(const Args&, const TileDesc&, int) {}
   __device__ static void load_a(const Args&, const TmaSet& tm, uint64_t* bar, uint8_t* s,
                                 const TileDesc& td, int kb) {
     tma_load_2d(&tm.m[0], bar, s, kb * BK, td.m0);
@@ -35,7 +36,8 @@ struct ModeNT {
                                 const TileDesc& td, int kb) {
     tma_load_2d(&tm.m[1], bar, s, kb * BK, td.e * a.n_per_expert + td.n0);
   }
-  __device__ static void epilogue(const Args& a, const TileDesc& td, uint32_t taddr, int r) {
+  __device__ static void epilogue(const Args& a, const TmaSet&, const TileDesc& td, uint32_t taddr, int r,
+                                  uint8_t*) {
     __nv_bfloat16* row = a.C + (size_t)(td.m0 + r) * a.ldc + td.n0;
     const bool live = r < td.rows;
 #pragma unroll 1
@@ -60,6 +62,7 @@ struct ModeTN {
   };
   __device__ static TileDesc tile(const Args& a, int t) { return a.tiles[t]; }
   __device__ static void before_loads(const Args&, const TileDesc&) {}
+  __device__ static void epilogue_prefetch(const Args&, const TileDesc&, int) {}
   __device__ static void load_a(const Args&, const TmaSet& tm, uint64_t* bar, uint8_t* s,
                                 const TileDesc& td, int kb) {
 #pragma unroll
@@ -72,7 +75,8 @@ struct ModeTN {
     for (int i = 0; i < BN / 64; ++i)
       tma_load_2d(&tm.m[1], bar, s + i * 8192, td.n0 + 64 * i, td.kb0 + kb * BK);
   }
-  __device__ static void epilogue(const Args& a, const TileDesc& td, uint32_t taddr, int r) {
+  __device__ static void epilogue(const Args& a, const TmaSet&, const TileDesc& td, uint32_t taddr, int r,
+                                  uint8_t*) {
     __nv_bfloat16* row = a.C + td.e * a.expert_stride + (size_t)(td.m0 + r) * a.ldc + td.n0;
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
@@ -94,7 +98,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                       int ntiles, int* cursor) {
   extern __shared__ uint8_t raw_smem[];
   uint8_t* base = smem_aligned(raw_smem);
-  GemmSmem* S = reinterpret_cast<GemmSmem*>(base + STAGES * (A_STAGE_BYTES + B_STAGE_BYTES));
+  GemmSmem* S = reinterpret_cast<GemmSmem*>(base + TILES_BYTES + EPI_BYTES);
   gemm_setup(S);
   if (threadIdx.x == 0) S->bcast = atomicAdd(cursor, 1);
   __syncthreads();
@@ -165,7 +169,7 @@ int eplab_grouped_gemm_nt(const void* A, const void* B, void* C, int M_total, in
                     cudaMemcpyHostToDevice, st);
     TmaSet tm;
     tm.m[0] = eplab_host::make_bf16_map(A, M_total, K, K, 64, BM);
-    tm.m[1] = tm.m[2] = tm.m[3] = eplab_host::make_bf16_map(B, (uint64_t)n_experts * N, K, K, 64, BN);
+    tm.m[1] = tm.m[2] = tm.m[3] = tm.m[4] = tm.m[5] = tm.m[6] = tm.m[7] = eplab_host::make_bf16_map(B, (uint64_t)n_experts * N, K, K, 64, BN);
     ModeNT::Args args{d_tiles, (__nv_bfloat16*)C, N, N};
     return launch_plain<ModeNT>(tm, args, d_tiles, (int)tiles.size(), d_cursor, st);
   } catch (...) {
@@ -200,7 +204,7 @@ int eplab_grouped_gemm_tn(const void* A, const void* B, void* C, int M_total, in
                     cudaMemcpyHostToDevice, st);
     TmaSet tm;
     tm.m[0] = eplab_host::make_bf16_map(A, M_total, NA, NA, 64, 64);
-    tm.m[1] = tm.m[2] = tm.m[3] = eplab_host::make_bf16_map(B, M_total, NB, NB, 64, 64);
+    tm.m[1] = tm.m[2] = tm.m[3] = tm.m[4] = tm.m[5] = tm.m[6] = tm.m[7] = eplab_host::make_bf16_map(B, M_total, NB, NB, 64, 64);
     ModeTN::Args args{d_tiles, (__nv_bfloat16*)C, NB, (long long)NA * NB};
     return launch_plain<ModeTN>(tm, args, d_tiles, (int)tiles.size(), d_cursor, st);
   } catch (...) {

@@ -151,8 +151,37 @@ __device__ __forceinline__ void even_slice(long long n, int parts, int i, long l
 }
 
 // ------------------------------------------------------------------ comm role
-// One warp per send item, 16-byte vector copies. ph = 0 forward (x), 1 backward
-// (dY; the warp also folds the gate gradient <dY_t, o_{t,j}> of every item it visits).
+// Row copy with U independent 16-byte loads in flight per lane (Guideline 7 / 13).
+template <int U>
+__device__ __forceinline__ void warp_copy_row(int4* __restrict__ dst, const int4* __restrict__ src,
+                                              int vecs, int lane) {
+  int c = lane;
+  for (; c + (U - 1) * 32 < vecs; c += U * 32) {
+    int4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ld_nc_v4(src + c + u * 32);
+#pragma unroll
+    for (int u = 0; u < U; ++u) dst[c + u * 32] = v[u];
+  }
+  for (; c < vecs; c += 32) dst[c] = ld_nc_v4(src + c);
+}
+
+__device__ __forceinline__ float dot8_bf16(const int4& a, const int4& b, float acc) {
+  const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&a);
+  const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 fa = __bfloat1622float2(ha[q]), fb = __bfloat1622float2(hb[q]);
+    acc = fmaf(fa.x, fb.x, acc);
+    acc = fmaf(fa.y, fb.y, acc);
+  }
+  return acc;
+}
+
+// One warp per send item, 16-byte vector copies. A warp resolves the metadata of
+// 32 consecutive schedule items at once (one lane each) and then moves their rows one by one.
+// ph = 0 forward (x), 1 backward (dY; the warp also folds the gate gradient <dY_t, o_{t,j}> of
+// every item it visits).
 __device__ void comm_task(const MkArgs& a, int task, int ph) {
   const Dims& d = a.d;
   const int k = d.topk, H = d.H, me = d.rank;
@@ -164,68 +193,88 @@ __device__ void comm_task(const MkArgs& a, int task, int ph) {
   const __nv_bfloat16* src_base = ph == 0 ? a.x : a.dy;
   const uint32_t flagv = a.epoch * 2 + ph;
   const int vecs = H / 8;
-  for (long long pi = lo + warp; pi < hi; pi += GEMM_THREADS / 32) {
-    const int i = a.p.sched[pi];
-    const int t = i / k, j = i - t * k;
-    const int e = a.p.topk_ids[i];
-    const int dst = e / d.epr, el = e - dst * d.epr;
-    const int slot = a.p.dst_slot[i];
-    bool primary = true;
-    if (relay_on)
-      for (int jj = 0; jj < k; ++jj) {
-        const int e2 = a.p.topk_ids[t * k + jj];
-        if (e2 / d.epr == dst && e2 - dst * d.epr < el) primary = false;
-      }
-    if (!primary && ph == 0) continue;
-    const int4* src = reinterpret_cast<const int4*>(src_base + (size_t)t * H);
-    const SymPtrs& P = a.peers.p[dst];
-    int4* dstrow = reinterpret_cast<int4*>(P.recv_x + (size_t)slot * H);
-    if (ph == 1) dstrow = reinterpret_cast<int4*>(P.recv_dy + (size_t)slot * H);
-    float gacc = 0.f;
-    const int4* orow = reinterpret_cast<const int4*>(a.peers.p[me].rep + (size_t)i * H);
-    for (int c = lane; c < vecs; c += 32) {
-      const int4 v = ld_nc_v4(src + c);
-      if (primary) dstrow[c] = v;
-      if (ph == 1) {
-        const int4 o = orow[c];
-        const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&v);
-        const __nv_bfloat162* ho = reinterpret_cast<const __nv_bfloat162*>(&o);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float2 fv = __bfloat1622float2(hv[q]), fo = __bfloat1622float2(ho[q]);
-          gacc = fmaf(fv.x, fo.x, gacc);
-          gacc = fmaf(fv.y, fo.y, gacc);
+  constexpr int NW = GEMM_THREADS / 32;
+  for (long long b0 = lo + (long long)warp * 32; b0 < hi; b0 += NW * 32) {
+    // ---- lane-parallel metadata of items b0 .. b0+31
+    const long long my = b0 + lane;
+    int mi = -1, mdst = 0, mslot = 0, mprim = 1;
+    if (my < hi) {
+      mi = a.p.sched[my];
+      const int e = a.p.topk_ids[mi];
+      mdst = e / d.epr;
+      mslot = a.p.dst_slot[mi];
+      if (relay_on) {
+        const int t = mi / k, el = e - mdst * d.epr;
+        for (int jj = 0; jj < k; ++jj) {
+          const int e2 = a.p.topk_ids[t * k + jj];
+          if (e2 / d.epr == mdst && e2 - mdst * d.epr < el) mprim = 0;
         }
       }
     }
-    if (ph == 1) {
+    const int cnt = (hi - b0) < 32 ? (int)(hi - b0) : 32;
+    for (int q = 0; q < cnt; ++q) {
+      const int i = __shfl_sync(0xffffffffu, mi, q);
+      const int dst = __shfl_sync(0xffffffffu, mdst, q);
+      const int slot = __shfl_sync(0xffffffffu, mslot, q);
+      const bool primary = __shfl_sync(0xffffffffu, mprim, q) != 0;
+      const int t = i / k, j = i - t * k;
+      if (!primary && ph == 0) continue;
+      const SymPtrs& P = a.peers.p[dst];
+      const int4* src = reinterpret_cast<const int4*>(src_base + (size_t)t * H);
+      int4* dstrow = reinterpret_cast<int4*>((ph == 0 ? P.recv_x : P.recv_dy) + (size_t)slot * H);
+      if (ph == 0) {
+        warp_copy_row<8>(dstrow, src, vecs, lane);
+      } else {
+        // dY row -> destination slot, and the gate gradient against the saved replica o_{t,j}
+        const int4* orow = reinterpret_cast<const int4*>(a.peers.p[me].rep + (size_t)i * H);
+        float gacc = 0.f;
+        int c = lane;
+        for (; c + 3 * 32 < vecs; c += 4 * 32) {
+          int4 v[4], o[4];
 #pragma unroll
-      for (int s = 16; s > 0; s >>= 1) gacc += __shfl_xor_sync(0xffffffffu, gacc, s);
-      if (lane == 0) a.dgate[i] = gacc;
-    }
-    if (!primary) continue;
-    if (ph == 0 && lane == 0) {
-      P.meta[slot] = SlotMeta{me, i, a.p.gate_w[i], -1};
-      if (relay_on)
-        for (int jj = 0; jj < k; ++jj) {
-          const int e2 = a.p.topk_ids[t * k + jj];
-          if (jj != j && e2 / d.epr == dst) {
-            const int s2 = a.p.dst_slot[t * k + jj];
-            P.meta[s2] = SlotMeta{me, t * k + jj, a.p.gate_w[t * k + jj], slot};
+          for (int u = 0; u < 4; ++u) {
+            v[u] = ld_nc_v4(src + c + u * 32);
+            o[u] = ld_nc_v4(orow + c + u * 32);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (primary) dstrow[c + u * 32] = v[u];
+            gacc = dot8_bf16(v[u], o[u], gacc);
           }
         }
-    }
-    __syncwarp();
-    if (lane == 0) {
-      __threadfence_system();
-      if (relay_on) {
-        st_release_sys(P.slot_flag + slot, flagv);
-        for (int jj = 0; jj < k; ++jj) {
-          const int e2 = a.p.topk_ids[t * k + jj];
-          if (jj != j && e2 / d.epr == dst) st_release_sys(P.slot_flag + a.p.dst_slot[t * k + jj], flagv);
+        for (; c < vecs; c += 32) {
+          const int4 v = ld_nc_v4(src + c), o = ld_nc_v4(orow + c);
+          if (primary) dstrow[c] = v;
+          gacc = dot8_bf16(v, o, gacc);
         }
-      } else {
-        red_release_sys_add(rg_counter(P, d, ph, a.par, slot >> 7), 1u);
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) gacc += __shfl_xor_sync(0xffffffffu, gacc, s);
+        if (lane == 0) a.dgate[i] = gacc;
+        if (!primary) continue;
+      }
+      if (ph == 0 && lane == 0) {
+        P.meta[slot] = SlotMeta{me, i, a.p.gate_w[i], -1};
+        if (relay_on)
+          for (int jj = 0; jj < k; ++jj) {
+            const int e2 = a.p.topk_ids[t * k + jj];
+            if (jj != j && e2 / d.epr == dst) {
+              const int s2 = a.p.dst_slot[t * k + jj];
+              P.meta[s2] = SlotMeta{me, t * k + jj, a.p.gate_w[t * k + jj], slot};
+            }
+          }
+      }
+      __syncwarp();  // orders every lane's row stores before lane 0's release (cumulative)
+      if (lane == 0) {
+        if (relay_on) {
+          st_release_sys(P.slot_flag + slot, flagv);
+          for (int jj = 0; jj < k; ++jj) {
+            const int e2 = a.p.topk_ids[t * k + jj];
+            if (jj != j && e2 / d.epr == dst)
+              st_release_sys(P.slot_flag + a.p.dst_slot[t * k + jj], flagv);
+          }
+        } else {
+          red_release_sys_add(rg_counter(P, d, ph, a.par, slot >> 7), 1u);
+        }
       }
     }
   }
@@ -253,11 +302,9 @@ __device__ void relay_task(const MkArgs& a, int task, int ph) {
       if (lane == 0) wait_eq_sys(me.slot_flag + s, flagv, a.timeout_ns, a.err, 10 + ph, s);
       __syncwarp();
       const int prim = me.meta[s].primary;
-      if (prim >= 0) {
-        const int4* src = reinterpret_cast<const int4*>(recv + (size_t)prim * d.H);
-        int4* dst = reinterpret_cast<int4*>(recv + (size_t)s * d.H);
-        for (int c = lane; c < vecs; c += 32) dst[c] = src[c];
-      }
+      if (prim >= 0)
+        warp_copy_row<8>(reinterpret_cast<int4*>(recv + (size_t)s * d.H),
+                         reinterpret_cast<const int4*>(recv + (size_t)prim * d.H), vecs, lane);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -287,31 +334,45 @@ __device__ void reduce_task(const MkArgs& a, int task, int ph) {
     __syncwarp();
     float w[16];
     for (int j = 0; j < k; ++j) w[j] = ph == 0 ? a.p.gate_w[t * k + j] : 1.0f;
-    for (int c = lane * 8; c < H; c += 256) {
-      float acc[8];
+    for (int c0 = lane * 8; c0 < H; c0 += 4 * 256) {
+      float acc[4][8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[u][q] = 0.f;
       for (int j = 0; j < k; ++j) {
-        const int4 v = *reinterpret_cast<const int4*>(rep + ((size_t)t * k + j) * H + c);
-        const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&v);
+        int4 v[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float2 f = __bfloat1622float2(hv[q]);
-          if (ph == 0) {
-            acc[2 * q] = fmaf(w[j], f.x, acc[2 * q]);
-            acc[2 * q + 1] = fmaf(w[j], f.y, acc[2 * q + 1]);
-          } else {
-            acc[2 * q] = acc[2 * q] + f.x;
-            acc[2 * q + 1] = acc[2 * q + 1] + f.y;
+        for (int u = 0; u < 4; ++u)
+          if (c0 + u * 256 < H)
+            v[u] = *reinterpret_cast<const int4*>(rep + ((size_t)t * k + j) * H + c0 + u * 256);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (c0 + u * 256 >= H) continue;
+          const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 f = __bfloat1622float2(hv[q]);
+            if (ph == 0) {
+              acc[u][2 * q] = fmaf(w[j], f.x, acc[u][2 * q]);
+              acc[u][2 * q + 1] = fmaf(w[j], f.y, acc[u][2 * q + 1]);
+            } else {
+              acc[u][2 * q] = acc[u][2 * q] + f.x;
+              acc[u][2 * q + 1] = acc[u][2 * q + 1] + f.y;
+            }
           }
         }
       }
-      int4 o;
-      o.x = (int)pack_bf16(acc[0], acc[1]);
-      o.y = (int)pack_bf16(acc[2], acc[3]);
-      o.z = (int)pack_bf16(acc[4], acc[5]);
-      o.w = (int)pack_bf16(acc[6], acc[7]);
-      *reinterpret_cast<int4*>(out + (size_t)t * H + c) = o;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (c0 + u * 256 >= H) continue;
+        int4 o;
+        o.x = (int)pack_bf16(acc[u][0], acc[u][1]);
+        o.y = (int)pack_bf16(acc[u][2], acc[u][3]);
+        o.z = (int)pack_bf16(acc[u][4], acc[u][5]);
+        o.w = (int)pack_bf16(acc[u][6], acc[u][7]);
+        *reinterpret_cast<int4*>(out + (size_t)t * H + c0 + u * 256) = o;
+      }
     }
   }
 }
@@ -333,8 +394,8 @@ struct ModeUp {
     const SymPtrs& me = a.peers.p[a.d.rank];
     wait_geq_sys(rg_counter(me, a.d, 0, a.par, td.m0 >> 7), (uint32_t)td.rows, a.timeout_ns, a.err,
                  30, td.m0 >> 7);
-    fence_proxy_async_global();
   }
+  __device__ static void epilogue_prefetch(const Args&, const TileDesc&, int) {}
   __device__ static void load_a(const Args&, const TmaSet& tm, uint64_t* bar, uint8_t* s,
                                 const TileDesc& td, int kb) {
     tma_load_2d(&tm.m[0], bar, s, kb * BK, td.m0);
@@ -345,26 +406,41 @@ struct ModeUp {
     tma_load_2d(&tm.m[1], bar, s, kb * BK, row);
     tma_load_2d(&tm.m[1], bar, s + 128 * 128, kb * BK, row + a.d.F);
   }
-  __device__ static void epilogue(const Args& a, const TileDesc& td, uint32_t taddr, int r) {
+  __device__ static void epilogue(const Args& a, const TmaSet& tm, const TileDesc& td,
+                                  uint32_t taddr, int r, uint8_t* stg) {
+    const uint32_t lane = r & 31;
     const bool live = r < td.rows;  // tcgen05.ld is warp-collective: every lane loads
-    const size_t m = (size_t)td.m0 + r;
+    const int row0 = td.m0 + (r & ~31);
     const int F = a.d.F;
 #pragma unroll 1
     for (int c = 0; c < 4; ++c) {
-      float g[32], u[32];
+      float g[32], u[32], h[32];
       acc_chunk(taddr, c, g);
       acc_chunk(taddr, 4 + c, u);
-      if (!live) continue;
-      __nv_bfloat16* gdst = a.gu + m * 2 * F + td.n0 + c * 32;
-      store_row_bf16_32(gdst, g);
-      store_row_bf16_32(gdst + F, u);
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const float gb = __bfloat162float(__float2bfloat16_rn(g[i]));
         const float ub = __bfloat162float(__float2bfloat16_rn(u[i]));
-        g[i] = silu_f(gb) * ub;
+        h[i] = silu_f(gb) * ub;
       }
-      store_row_bf16_32(a.hact + m * F + td.n0 + c * 32, g);
+      stage_acquire(lane);
+      if (live) {
+        stage_row(stg, lane, g);
+        stage_row(stg + EPI_TILE_BYTES, lane, u);
+        stage_row(stg + 2 * EPI_TILE_BYTES, lane, h);
+      } else {
+        stage_zero_row(stg, lane);
+        stage_zero_row(stg + EPI_TILE_BYTES, lane);
+        stage_zero_row(stg + 2 * EPI_TILE_BYTES, lane);
+      }
+      stage_release();
+      if (lane == 0) {
+        const int col = td.n0 + c * 32;
+        tma_store_2d(&tm.m[4], stg, col, row0);                       // GU gate half
+        tma_store_2d(&tm.m[4], stg + EPI_TILE_BYTES, F + col, row0);  // GU up half
+        tma_store_2d(&tm.m[5], stg + 2 * EPI_TILE_BYTES, col, row0);  // h
+        tma_store_commit();
+      }
     }
   }
   template <class A>
@@ -393,6 +469,7 @@ __device__ __forceinline__ void push_rows(const MkArgs& a, const TileDesc& td, u
 struct ModeDown {
   using Args = MkArgs;
   static constexpr bool HAS_TILE_DONE = false;
+  __device__ static void epilogue_prefetch(const Args&, const TileDesc&, int) {}
   __device__ static int a_mn(const TileDesc&) { return 0; }
   __device__ static int b_mn(const TileDesc&) { return 0; }
   __device__ static TileDesc tile(const Args& a, int t) {
@@ -407,12 +484,40 @@ struct ModeDown {
                                 const TileDesc& td, int kb) {
     tma_load_2d(&tm.m[1], bar, s, kb * BK, td.e * a.d.H + td.n0);
   }
-  __device__ static void epilogue(const Args& a, const TileDesc& td, uint32_t taddr, int r) {
+  __device__ static void epilogue(const Args& a, const TmaSet&, const TileDesc& td, uint32_t taddr,
+                                  int r, uint8_t*) {
     push_rows(a, td, taddr, r, 0);
   }
   template <class A>
   __device__ static void tile_done(const A&, const TileDesc&) {}
 };
+
+// Weight-gradient tile (128 x 256 fp32 in TMEM) -> bf16 through the warp's three staging tiles
+// (round robin, two store groups in flight) and TMA stores into dW viewed as [epr*NO][KO].
+__device__ __forceinline__ void wgrad_store(const CUtensorMap* map, const TileDesc& td, int NO,
+                                            uint32_t taddr, int r, uint8_t* stg) {
+  const uint32_t lane = r & 31;
+  const int row0 = td.e * NO + td.m0 + (r & ~31);
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    float v[32];
+    if (td.nkb > 0) {
+      acc_chunk(taddr, c, v);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = 0.f;
+    }
+    uint8_t* buf = stg + (c % 3) * EPI_TILE_BYTES;
+    if (lane == 0) tma_store_wait_read<2>();
+    __syncwarp();
+    stage_row(buf, lane, v);
+    stage_release();
+    if (lane == 0) {
+      tma_store_2d(map, buf, td.n0 + c * 32, row0);
+      tma_store_commit();
+    }
+  }
+}
 
 // Backward: down-dgrad tiles then down-wgrad tiles.
 //   dgrad : A = recv_dy (K-major over H), B = W_down[e] as [H rows = K][F cols] (MN-major).
@@ -440,7 +545,17 @@ struct ModeDgradDown {
       wait_geq_sys(a.wg_cnt + td.e * (a.d.F / BN) + td.pad0, (uint32_t)a.p.mblocks[td.e],
                    a.timeout_ns, a.err, 32, td.e * 1000 + td.pad0);
     }
-    fence_proxy_async_global();
+  }
+  // dgrad tiles: pull this row's saved g, u (the SwiGLU backward inputs) toward L2 before the
+  // accumulator is ready
+  __device__ static void epilogue_prefetch(const Args& a, const TileDesc& td, int r) {
+    if (td.pad1 || r >= td.rows) return;
+    const char* g = reinterpret_cast<const char*>(a.gu + ((size_t)td.m0 + r) * 2 * a.d.F + td.n0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(g + i * 128));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(g + (size_t)a.d.F * 2 + i * 128));
+    }
   }
   __device__ static void load_a(const Args&, const TmaSet& tm, uint64_t* bar, uint8_t* s,
                                 const TileDesc& td, int kb) {
@@ -464,24 +579,16 @@ struct ModeDgradDown {
         tma_load_2d(&tm.m[3], bar, s + i * 8192, td.n0 + 64 * i, td.kb0 + kb * BK);
     }
   }
-  __device__ static void epilogue(const Args& a, const TileDesc& td, uint32_t taddr, int r) {
+  __device__ static void epilogue(const Args& a, const TmaSet& tm, const TileDesc& td,
+                                  uint32_t taddr, int r, uint8_t* stg) {
     const int F = a.d.F;
-    if (td.pad1) {  // weight gradient tile
-      __nv_bfloat16* row = a.dw_down + ((size_t)td.e * a.d.H + td.m0 + r) * F + td.n0;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        float v[32];
-        if (td.nkb > 0) {
-          acc_chunk(taddr, c, v);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = 0.f;
-        }
-        store_row_bf16_32(row + c * 32, v);
-      }
+    if (td.pad1) {  // weight-gradient tile
+      wgrad_store(&tm.m[6], td, a.d.H, taddr, r, stg);
       return;
     }
+    const uint32_t lane = r & 31;
     const size_t m = (size_t)td.m0 + r;
+    const int row0 = td.m0 + (r & ~31);
     const bool live = r < td.rows;
     const float w = live ? a.peers.p[a.d.rank].meta[m].w : 0.f;
 #pragma unroll 1
@@ -489,33 +596,47 @@ struct ModeDgradDown {
       float v[32];
       acc_chunk(taddr, c, v);
       const int f0 = td.n0 + c * 32;
-      __nv_bfloat16* dg = a.dgu + m * 2 * F + f0;
-      __nv_bfloat16* hwr = a.hw + m * F + f0;
-      if (!live) {
-        store_zero_32(dg);
-        store_zero_32(dg + F);
-        store_zero_32(hwr);
-        continue;
-      }
-      float g[32], u[32];
-      load_row_bf16_32(a.gu + m * 2 * F + f0, g);
-      load_row_bf16_32(a.gu + m * 2 * F + F + f0, u);
-      float du[32], hv[32];
+      float g[32], u[32], du[32], hv[32];
+      if (live) {
+        load_row_bf16_32(a.gu + m * 2 * F + f0, g);
+        load_row_bf16_32(a.gu + m * 2 * F + F + f0, u);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float dh = w * v[i];
-        const float s = 1.0f / (1.0f + __expf(-g[i]));
-        const float si = g[i] * s;
-        const float ds = s * (1.0f + g[i] * (1.0f - s));
-        const float h = __bfloat162float(__float2bfloat16_rn(si * u[i]));
-        v[i] = dh * u[i] * ds;
-        du[i] = dh * si;
-        hv[i] = w * h;
+        for (int i = 0; i < 32; ++i) {
+          const float dh = w * v[i];
+          const float s = 1.0f / (1.0f + __expf(-g[i]));
+          const float si = g[i] * s;
+          const float ds = s * (1.0f + g[i] * (1.0f - s));
+          const float h = __bfloat162float(__float2bfloat16_rn(si * u[i]));
+          v[i] = dh * u[i] * ds;
+          du[i] = dh * si;
+          hv[i] = w * h;
+        }
       }
-      store_row_bf16_32(dg, v);
-      store_row_bf16_32(dg + F, du);
-      store_row_bf16_32(hwr, hv);
+      stage_acquire(lane);
+      if (live) {
+        stage_row(stg, lane, v);
+        stage_row(stg + EPI_TILE_BYTES, lane, du);
+        stage_row(stg + 2 * EPI_TILE_BYTES, lane, hv);
+      } else {  // zero padding rows: the K padding of the transposed weight-gradient GEMM
+        stage_zero_row(stg, lane);
+        stage_zero_row(stg + EPI_TILE_BYTES, lane);
+        stage_zero_row(stg + 2 * EPI_TILE_BYTES, lane);
+      }
+      stage_release();
+      if (lane == 0) {
+        tma_store_2d(&tm.m[4], stg, f0, row0);                       // dGU gate half
+        tma_store_2d(&tm.m[4], stg + EPI_TILE_BYTES, F + f0, row0);  // dGU up half
+        tma_store_2d(&tm.m[5], stg + 2 * EPI_TILE_BYTES, f0, row0);  // HW
+        tma_store_commit();
+      }
     }
+    // the weight-gradient tiles of this (expert, f-block) read HW / dGU through TMA: complete
+    // the stores before tile_done publishes the count
+    if (lane == 0) {
+      tma_store_wait<0>();
+      fence_proxy_async_global();
+    }
+    __syncwarp();
   }
   __device__ static void tile_done(const Args& a, const TileDesc& td) {
     if (td.pad1) return;
@@ -530,6 +651,7 @@ struct ModeDgradDown {
 struct ModeDgradUp {
   using Args = MkArgs;
   static constexpr bool HAS_TILE_DONE = false;
+  __device__ static void epilogue_prefetch(const Args&, const TileDesc&, int) {}
   __device__ static int n_dgrad(const Args& a) { return a.p.mblock_pre[a.d.epr] * (a.d.H / BN); }
   __device__ static int a_mn(const TileDesc& td) { return td.pad1; }
   __device__ static int b_mn(const TileDesc&) { return 1; }
@@ -561,23 +683,13 @@ struct ModeDgradUp {
         tma_load_2d(&tm.m[3], bar, s + i * 8192, td.n0 + 64 * i, td.kb0 + kb * BK);
     }
   }
-  __device__ static void epilogue(const Args& a, const TileDesc& td, uint32_t taddr, int r) {
+  __device__ static void epilogue(const Args& a, const TmaSet& tm, const TileDesc& td,
+                                  uint32_t taddr, int r, uint8_t* stg) {
     if (!td.pad1) {
       push_rows(a, td, taddr, r, 1);
       return;
     }
-    __nv_bfloat16* row = a.dw_up + ((size_t)td.e * 2 * a.d.F + td.m0 + r) * a.d.H + td.n0;
-#pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
-      float v[32];
-      if (td.nkb > 0) {
-        acc_chunk(taddr, c, v);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = 0.f;
-      }
-      store_row_bf16_32(row + c * 32, v);
-    }
+    wgrad_store(&tm.m[6], td, 2 * a.d.F, taddr, r, stg);
   }
   template <class A>
   __device__ static void tile_done(const A&, const TileDesc&) {}
@@ -590,7 +702,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     megakernel(const __grid_constant__ TmaSet tm, const __grid_constant__ MkArgs a) {
   extern __shared__ uint8_t raw_smem[];
   uint8_t* base = smem_aligned(raw_smem);
-  GemmSmem* S = reinterpret_cast<GemmSmem*>(base + STAGES * (A_STAGE_BYTES + B_STAGE_BYTES));
+  GemmSmem* S = reinterpret_cast<GemmSmem*>(base + TILES_BYTES + EPI_BYTES);
   const int ph = (KIND >= 2) ? 1 : 0;
   const bool has_pre = (KIND == 0 || KIND == 2);
   const bool has_post = (KIND == 1 || KIND == 3);

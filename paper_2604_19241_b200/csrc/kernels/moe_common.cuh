@@ -85,9 +85,10 @@ struct PlanDev {
   int* scalars;             // [0]=M_used rows (aligned), [1]=n_rowgroups, [2]=recv total
 };
 
-// Up to four tensor maps travel as one __grid_constant__ kernel parameter.
+// Tensor maps travel as one __grid_constant__ kernel parameter: m[0..3] operand loads,
+// m[4..7] epilogue stores (box 32x32, 64B swizzle).
 struct TmaSet {
-  CUtensorMap m[4];
+  CUtensorMap m[8];
 };
 
 // Device timeline record (one per task): %globaltimer interval, SM, role, task id.
@@ -131,6 +132,7 @@ struct MkArgs {
   int n_disp, n_relay, n_red;
   unsigned long long timeout_ns;
   Timeline tl;
+  int dbg;  // debug bits (experiments only): 1 = skip epilogue stores of the up GEMM
 };
 
 }  // namespace eplab_dev

@@ -193,11 +193,17 @@ class EpMoE:
             out = dict(dx=torch.empty(n, self.H, dtype=torch.bfloat16, device=dev),
                        dw_up=torch.empty_like(w_up), dw_down=torch.empty_like(w_down),
                        dgate=torch.empty(n, self.k, dtype=torch.float32, device=dev))
+        self._dispatch_bwd(dy, w_down, out, stream)
+        self._combine_bwd(w_up, out, stream)
+        return out
+
+    def _dispatch_bwd(self, dy, w_down, out, stream=None):
         _check(lib().eplab_dispatch_group_gemm_bwd(self.h, _ptr(dy), _ptr(w_down), _ptr(out["dw_down"]),
                                                    _ptr(out["dgate"]), _stream(stream)))
+
+    def _combine_bwd(self, w_up, out, stream=None):
         _check(lib().eplab_group_gemm_combine_bwd(self.h, _ptr(w_up), _ptr(out["dx"]), _ptr(out["dw_up"]),
                                                   _stream(stream)))
-        return out
 
     def step_host(self, ids_h, gw_h, x_h, dy_h, w_up, w_down, y_h, dx_h, dgate_h, dw_up, dw_down,
                   stream=None):

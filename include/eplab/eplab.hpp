@@ -1,0 +1,222 @@
+// eplab C++ host API of the B200 build (namespace eplab), re-implemented from scratch so that
+// callers written against the reference's headers (/root/reference/proj/src/eplab/*.hpp) find
+// the same types and entry points. Device data-path entry points live in eplab_b200.h.
+//
+//   types.hpp:16-82      HardwareSpec, MoEShape, TuneConfig, RoutingInstance, validate_*
+//   routing.hpp:15       sample_routing
+//   token_map.hpp:22-93  local_stable_sort, compute_global_offsets, build_global_token_map,
+//                        build_send_schedule
+//   traffic.hpp:28-51    distinct_rank_distribution, volume_expected, volume_exact
+//   perf_model.hpp:38-62 effective_bandwidth ... predict_latency (reference-compatible)
+//   tuner.hpp:16-82      enumerate_space, search, TuneCache
+// B200 additions: b200_hardware(), predict_layer() (fwd+bwd model of the MegaKernels built
+// here, incl. the relay-off AllToAll mode), search_layer().
+#pragma once
+#include <cstdint>
+#include <functional>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace eplab {
+
+class ValidationError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class DeadlockError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+struct HardwareSpec {
+  std::string name;
+  int n_sm = 0;
+  double p_peak = 0;       // bf16 FLOP/s
+  double bw_hbm = 0;       // B/s
+  double bw_nvl = 0;       // B/s per direction
+  double w_sat = 1024;     // warps to saturate a link
+  double tau_sync = 2e-6;  // per-tile synchronisation, s
+  int world_size = 1;
+};
+
+struct MoEShape {
+  std::string name;
+  int h_dim = 0, h_inter = 0, n_exp = 0, topk = 0;
+  long long n_tok = 0;  // tokens per rank
+  long long s_tok = 0;  // bytes per token row (0: 2*h_dim)
+  int b_m = 128, b_n = 256;
+  std::map<int, double> mu_table = {{8, 0.7}, {16, 0.65}, {32, 0.6}};
+  long long token_bytes() const { return s_tok > 0 ? s_tok : 2LL * h_dim; }
+  int experts_per_rank(int world) const { return n_exp / world; }
+};
+
+struct TuneConfig {
+  int n_disp = 0, n_relay = 0, n_comb = 0, n_red = 0, w = 0;
+  bool operator==(const TuneConfig&) const = default;
+};
+
+struct RoutingInstance {
+  int world = 0, n_exp = 0, topk = 0;
+  long long n_tok = 0;
+  std::uint64_t seed = 0;
+  std::vector<std::vector<int>> selected_experts;  // [rank][t*topk+j]
+  std::vector<std::vector<float>> gate_weights;
+  int expert_at(int r, long long t, int j) const { return selected_experts[r][t * topk + j]; }
+  float weight_at(int r, long long t, int j) const { return gate_weights[r][t * topk + j]; }
+};
+
+HardwareSpec validate_hardware(HardwareSpec spec);
+std::pair<MoEShape, HardwareSpec> validate_shape(MoEShape shape, HardwareSpec spec);
+void validate_tune_config(const TuneConfig& cfg, const HardwareSpec& spec);
+void validate_routing(const RoutingInstance& routing);
+
+RoutingInstance sample_routing(const MoEShape& shape, int world, std::uint64_t seed);
+
+// --------------------------------------------------------------- token map (host mirror)
+struct LocalSortResult {
+  std::vector<long long> m_loc, expert_counts, expert_offsets;
+};
+LocalSortResult local_stable_sort(const std::vector<int>& selected, long long n_tok, int topk,
+                                  int n_exp);
+struct GlobalOffsets {
+  int world = 0, experts_per_rank = 0;
+  std::vector<long long> data;  // [dst][e_loc][src]
+  long long at(int dst, int e_loc, int src) const {
+    return data[((size_t)dst * experts_per_rank + e_loc) * world + src];
+  }
+};
+GlobalOffsets compute_global_offsets(const std::vector<std::vector<long long>>& counts, int world,
+                                     int n_exp);
+struct MapEntry {
+  int target_rank = 0, local_expert = 0;
+  long long offset = 0;
+  bool operator==(const MapEntry&) const = default;
+};
+struct GlobalTokenMap {
+  int rank = 0, topk = 0, world = 0, experts_per_rank = 0;
+  long long n_tok = 0;
+  std::vector<MapEntry> entries;
+  std::vector<long long> recv_totals, recv_segment_base;
+  const MapEntry& at(long long t, int j) const { return entries[t * topk + j]; }
+};
+std::vector<GlobalTokenMap> build_global_token_map(const RoutingInstance& routing);
+struct SendItem {
+  long long token = 0;
+  int slot = 0, dst_rank = 0, dst_expert = 0;
+  long long dst_offset = 0;
+  bool operator==(const SendItem&) const = default;
+};
+struct SendSchedule {
+  int rank = 0;
+  std::vector<SendItem> items;
+};
+SendSchedule build_send_schedule(const GlobalTokenMap& map);
+
+// --------------------------------------------------------------- traffic
+struct DistinctRankDistribution {
+  int world = 0, topk = 0;
+  std::vector<unsigned __int128> numerators;  // index x-1
+  unsigned __int128 denominator = 1;
+  std::vector<double> probs;
+  double expectation = 0, expected_saving_fraction = 0;
+  double prob(int x) const { return probs[x - 1]; }
+};
+DistinctRankDistribution distinct_rank_distribution(int world, int topk);
+enum class SelfRankAccounting { IncludeSelf, RemoteOnly };
+struct TrafficReport {
+  double v_allgather = 0, v_alltoall = 0, v_megakernel_nvl = 0, v_megakernel_hbm = 0;
+};
+TrafficReport volume_expected(const MoEShape& shape, const HardwareSpec& spec,
+                              SelfRankAccounting acc = SelfRankAccounting::IncludeSelf);
+TrafficReport volume_exact(const RoutingInstance& routing, const MoEShape& shape,
+                           const HardwareSpec& spec,
+                           SelfRankAccounting acc = SelfRankAccounting::IncludeSelf);
+// Exact E[#distinct remote ranks] for top-k drawn WITHOUT replacement from n_exp experts
+// spread evenly over `world` ranks.
+double expected_remote_ranks(int n_exp, int world, int topk);
+
+// --------------------------------------------------------------- perf model (reference Alg. 2)
+enum class ResidualScaling { AsPrinted, Redistributed };
+struct LatencyBreakdown {
+  double t_up = 0, t_down = 0, l_swiglu = 0, l_disp = 0, l_up = 0, l_comb = 0, l_down = 0,
+         t_red = 0, l_s1 = 0, l_s2 = 0, l_total = 0;
+  long long n_tiles_up = 0, n_tiles_down = 0;
+  double w_gap = 0, w_red = 0, w_rem = 0;
+};
+double effective_bandwidth(int n_sm_active, int w, double beta, double w_sat);
+double calc_gemm_block_time(const HardwareSpec& spec, const MoEShape& shape, long long k_dim, int w);
+double calc_swiglu(const MoEShape& shape, const HardwareSpec& spec, long long expanded_tokens);
+double calc_disp_lat(const TrafficReport& traffic, const HardwareSpec& spec, const TuneConfig& cfg);
+double calc_comp_lat(long long n_tiles, double t_block, int n_comp_sms);
+std::pair<double, double> calc_comb_lat(const TrafficReport& traffic, const HardwareSpec& spec,
+                                        const TuneConfig& cfg);
+long long tiles_up(const MoEShape& shape, int world);
+long long tiles_down(const MoEShape& shape, int world);
+LatencyBreakdown predict_latency(const MoEShape& shape, const HardwareSpec& spec,
+                                 const TuneConfig& cfg, const TrafficReport& traffic,
+                                 ResidualScaling mode = ResidualScaling::AsPrinted);
+
+// --------------------------------------------------------------- B200 model of the MegaKernels
+// Calibrated constants of this implementation on B200 (DESIGN.md §Performance model).
+struct B200Calib {
+  double mu_longk = 0.88;     // tensor-pipe efficiency of GEMM tiles with K >= 8192
+  double mu_shortk = 0.78;    // ... with K < 8192 (epilogue-heavier per FLOP)
+  double comm_bw_per_sm = 40e9;   // B/s one comm CTA sustains on row copies (8 warps)
+  double relay_bw_per_sm = 40e9;  // B/s one relay CTA sustains on HBM copies
+  double reduce_bw = 3.5e12;      // B/s of the reduce role when all SMs join (HBM bound)
+  double launch = 6e-6;           // per MegaKernel launch + prologue
+};
+struct LayerPrediction {
+  double fwd_dispatch = 0, fwd_combine = 0, bwd_dispatch = 0, bwd_combine = 0, total = 0;
+  double t_gemm_bound = 0, t_nvl_bound = 0;  // roofline terms
+};
+HardwareSpec b200_hardware(int world, double p_peak = 1408.1e12, double bw_hbm = 6468.9e9,
+                           double bw_nvl = 770e9);
+// cfg.n_relay == 0 selects the AllToAll-style primitive (every replica crosses NVLink).
+LayerPrediction predict_layer(const MoEShape& shape, const HardwareSpec& spec,
+                              const TuneConfig& cfg, const B200Calib& calib = {});
+
+// --------------------------------------------------------------- tuner
+struct SearchSpace {
+  int n_sm = 0;
+  std::vector<int> disp_choices, comb_choices, red_choices, warp_choices;
+  long long raw_grid_size = 0, enumerated_count = 0;
+  static std::vector<int> relay_choices(int n_disp);
+};
+SearchSpace enumerate_space(const HardwareSpec& spec, const MoEShape& shape);
+void for_each_candidate(const SearchSpace& space, bool feasible_only,
+                        const std::function<void(const TuneConfig&)>& fn);
+struct TuneResult {
+  TuneConfig best;
+  double l_min = 0;
+  long long evaluated = 0;
+  double wall_seconds = 0;
+  LatencyBreakdown breakdown;
+};
+using LatencyFn = std::function<double(const TuneConfig&)>;
+TuneResult search_with(const HardwareSpec& spec, const MoEShape& shape, const LatencyFn& eval,
+                       int n_workers = 0);
+TuneResult search(const HardwareSpec& spec, const MoEShape& shape, const TrafficReport& traffic,
+                  int n_workers = 0, ResidualScaling mode = ResidualScaling::AsPrinted);
+// B200: minimise predict_layer().total over (n_disp, n_relay in {0} U relay_choices, n_red) at
+// the w this build implements (8).
+TuneResult search_layer(const HardwareSpec& spec, const MoEShape& shape, int n_workers = 0,
+                        const B200Calib& calib = {});
+long long token_bucket(long long n_tok);
+class TuneCache {
+ public:
+  TuneResult lookup(const HardwareSpec& spec, const MoEShape& shape, long long n_tok,
+                    int n_workers = 0, ResidualScaling mode = ResidualScaling::AsPrinted);
+  long long search_invocations() const { return invocations_; }
+  size_t size() const { return entries_.size(); }
+  void save(const std::string& path) const;
+  void load(const std::string& path);
+
+ private:
+  std::map<std::tuple<std::string, std::string, long long>, TuneResult> entries_;
+  long long invocations_ = 0;
+};
+
+}  // namespace eplab

@@ -163,6 +163,68 @@ EPLAB_API void* eplab_buffer(eplab_ctx* ctx, const char* name);
 EPLAB_API int eplab_timeline_enable(eplab_ctx* ctx, int cap);
 EPLAB_API int eplab_timeline_export(eplab_ctx* ctx, const char* path, double* overlap_frac);
 
+/* ------------------------------------------------ host model API (C view of eplab::, eplab.hpp) */
+
+typedef struct {
+  int n_sm;
+  double p_peak, bw_hbm, bw_nvl, w_sat, tau_sync;
+  int world_size;
+} eplab_hw;                          /* HardwareSpec, types.hpp:16-25 */
+typedef struct {
+  int h_dim, h_inter, n_exp, topk;
+  long long n_tok, s_tok;
+  int b_m, b_n;
+  int mu_n;
+  int mu_w[8];
+  double mu_v[8];
+} eplab_shape;                       /* MoEShape, types.hpp:28-42 */
+typedef struct {
+  double v_allgather, v_alltoall, v_megakernel_nvl, v_megakernel_hbm;
+} eplab_traffic;                     /* TrafficReport, traffic.hpp:39-44 */
+typedef struct {
+  double t_up, t_down, l_swiglu, l_disp, l_up, l_comb, l_down, t_red, l_s1, l_s2, l_total;
+  long long n_tiles_up, n_tiles_down;
+  double w_gap, w_red, w_rem;
+} eplab_breakdown;                   /* LatencyBreakdown, perf_model.hpp:17-35 */
+typedef struct {
+  double mu_longk, mu_shortk, comm_bw_per_sm, relay_bw_per_sm, reduce_bw, launch;
+} eplab_b200_calib;                  /* B200 calibration of this build's MegaKernels */
+typedef struct {
+  double fwd_dispatch, fwd_combine, bwd_dispatch, bwd_combine, total, t_gemm_bound, t_nvl_bound;
+} eplab_layer_prediction;
+
+/* sample_routing (routing.hpp:15): sel int32 / gw fp32, rank-major [world][n_tok*topk]. */
+EPLAB_API int eplab_sample_routing(int n_exp, int topk, long long n_tok, int world, uint64_t seed,
+                                   int32_t* sel, float* gw);
+/* build_global_token_map (token_map.hpp:68) on the host, all ranks; outputs rank-major. */
+EPLAB_API int eplab_host_token_map(const int32_t* sel, int world, int n_exp, long long n_tok,
+                                   int topk, int32_t* target_rank, int32_t* local_expert,
+                                   int64_t* offset, int64_t* recv_totals, int64_t* seg_base);
+/* build_send_schedule (token_map.hpp:88) for one rank. */
+EPLAB_API int eplab_host_send_schedule(const int32_t* sel, int world, int n_exp, long long n_tok,
+                                       int topk, int rank, int64_t* item_token, int32_t* item_slot,
+                                       int32_t* item_dst_rank, int32_t* item_dst_expert,
+                                       int64_t* item_dst_offset);
+/* volume_expected (traffic.hpp:46); remote_only = SelfRankAccounting::RemoteOnly. */
+EPLAB_API int eplab_volume_expected(const eplab_shape* s, const eplab_hw* h, int remote_only,
+                                    eplab_traffic* out);
+/* predict_latency (perf_model.hpp:60), reference-compatible forward model. */
+EPLAB_API int eplab_predict_latency(const eplab_shape* s, const eplab_hw* h,
+                                    const eplab_tune_config* c, const eplab_traffic* t,
+                                    int redistributed, eplab_breakdown* out);
+/* search (tuner.hpp:49): exhaustive, deterministic for any worker count. */
+EPLAB_API int eplab_search(const eplab_shape* s, const eplab_hw* h, const eplab_traffic* t,
+                           int n_workers, int redistributed, eplab_tune_config* best,
+                           double* l_min, long long* evaluated);
+/* B200 fwd+bwd model of this build's MegaKernels (calib NULL = built-in constants). */
+EPLAB_API int eplab_predict_layer(const eplab_shape* s, const eplab_hw* h,
+                                  const eplab_tune_config* c, const eplab_b200_calib* calib,
+                                  eplab_layer_prediction* out);
+/* Minimises eplab_predict_layer over (n_disp, n_relay incl. 0 = AllToAll mode). */
+EPLAB_API int eplab_search_layer(const eplab_shape* s, const eplab_hw* h,
+                                 const eplab_b200_calib* calib, eplab_tune_config* best,
+                                 double* l_min, long long* evaluated);
+
 #ifdef __cplusplus
 }
 #endif

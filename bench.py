@@ -198,6 +198,8 @@ def run_ours(args):
     if world > 1:
         layer.connect_distributed()
     cfg = choose_config(H, F, E, k, T, world)
+    if args.tune:
+        cfg = M.TuneConfig(*[int(v) for v in args.tune.split(",")])
     layer.set_tune_config(cfg)
     y = torch.empty(T, H, device="cuda", dtype=torch.bfloat16)
     out = dict(dx=torch.empty(T, H, dtype=torch.bfloat16, device="cuda"), dw_up=torch.empty_like(w_up),
@@ -334,6 +336,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tune", default="", help="override n_disp,n_relay,n_comb,n_red,w")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

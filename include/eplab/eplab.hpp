@@ -163,9 +163,9 @@ LatencyBreakdown predict_latency(const MoEShape& shape, const HardwareSpec& spec
 struct B200Calib {
   double mu_longk = 0.88;     // tensor-pipe efficiency of GEMM tiles with K >= 8192
   double mu_shortk = 0.78;    // ... with K < 8192 (epilogue-heavier per FLOP)
-  double comm_bw_per_sm = 40e9;   // B/s one comm CTA sustains on row copies (8 warps)
-  double relay_bw_per_sm = 40e9;  // B/s one relay CTA sustains on HBM copies
-  double reduce_bw = 3.5e12;      // B/s of the reduce role when all SMs join (HBM bound)
+  double comm_bw_per_sm = 16e9;   // B/s one comm CTA sustains (TMA bulk row copies, measured)
+  double relay_bw_per_sm = 16e9;  // B/s one relay CTA sustains on HBM copies
+  double reduce_bw = 3.0e12;      // B/s of the reduce role when all SMs join (HBM bound)
   double launch = 6e-6;           // per MegaKernel launch + prologue
 };
 struct LayerPrediction {

@@ -58,6 +58,14 @@ struct GemmSmem {
   int ring[RING];
   uint32_t tmem_base;
   int bcast;
+  // comm role (runs before the CTA enters the GEMM roles; reuses the stage buffers)
+  uint64_t cbar[48];      // one mbarrier per bulk-copy slot
+  uint64_t cphase;        // parity bit per slot (carried across comm tasks)
+  int cpos[48];           // round position of the item held by each slot
+  int crel[64];           // round position by load sequence (release ring)
+  int citem[256];         // per-round item metadata
+  int cslot[256];
+  int cdst[256];
 };
 
 // Epilogue staging: per epilogue warp three 32x32 bf16 tiles (64 B rows, 64B-swizzled) that the

@@ -50,6 +50,11 @@ __device__ __forceinline__ void report_timeout(int* err, int site, uint32_t targ
     err[4] = where;
   }
 }
+// Once any watchdog has fired (err[0] != 0) every later wait gives up at once, so a protocol
+// failure costs one timeout, not one per waiting tile.
+__device__ __forceinline__ bool aborted(const int* err) {
+  return *reinterpret_cast<const volatile int*>(err) != 0;
+}
 __device__ __forceinline__ void wait_geq_sys(const uint32_t* p, uint32_t target,
                                              unsigned long long timeout, int* err, int site = 0,
                                              int where = 0) {
@@ -57,6 +62,7 @@ __device__ __forceinline__ void wait_geq_sys(const uint32_t* p, uint32_t target,
   const unsigned long long t0 = globaltimer();
   uint32_t v;
   while ((v = ld_acquire_sys(p)) < target) {
+    if (aborted(err)) return;
     if (globaltimer() - t0 > timeout) {
       report_timeout(err, site, target, v, where);
       return;
@@ -70,6 +76,7 @@ __device__ __forceinline__ void wait_eq_sys(const uint32_t* p, uint32_t want,
   const unsigned long long t0 = globaltimer();
   uint32_t v;
   while ((v = ld_acquire_sys(p)) != want) {
+    if (aborted(err)) return;
     if (globaltimer() - t0 > timeout) {
       report_timeout(err, site, want, v, where);
       return;
@@ -178,11 +185,80 @@ __device__ __forceinline__ float dot8_bf16(const int4& a, const int4& b, float a
   return acc;
 }
 
-// One warp per send item, 16-byte vector copies. A warp resolves the metadata of
-// 32 consecutive schedule items at once (one lane each) and then moves their rows one by one.
-// ph = 0 forward (x), 1 backward (dY; the warp also folds the gate gradient <dY_t, o_{t,j}> of
-// every item it visits).
-__device__ void comm_task(const MkArgs& a, int task, int ph) {
+// Comm role. The rows of a slice of the priority-ordered send schedule (token_map.cpp:108-126)
+// are moved by the TMA bulk-copy engine: one elected thread streams them global -> smem slot ->
+// destination slot (a peer's symmetric receive buffer over NVLink, or the local one), keeping
+// NSLOT rows in flight through the CTA's (idle during this phase) GEMM stage buffers. A row's
+// scoreboard release (rowgroup counter, or per-slot flags for the relay) is issued only after its
+// bulk store has completed. ph = 0 forward (x rows), 1 backward (dY rows; warps 1..7 meanwhile
+// fold the gate gradient <dY_t, o_{t,j}> of every item of the slice).
+template <int NSLOT>
+__device__ void comm_pipeline(const MkArgs& a, int ph, GemmSmem* S, uint8_t* sbuf, int cnt) {
+  constexpr int L = NSLOT / 2;               // loads run L rows ahead of stores
+  constexpr uint32_t SLOT = 196608 / NSLOT;  // bytes per slot
+  const Dims& d = a.d;
+  const int k = d.topk, H = d.H;
+  const uint32_t row_bytes = (uint32_t)H * 2;
+  const __nv_bfloat16* src_base = ph == 0 ? a.x : a.dy;
+  uint64_t par = S->cphase;
+  int n_loaded = 0, n_stored = 0, n_released = 0;
+  // Publish items [n_released, upto) whose bulk stores have completed: one async-proxy fence and
+  // one system-scope release fence for the batch, then relaxed scoreboard updates (the fence +
+  // relaxed-store release pattern), rowgroup counts aggregated over consecutive items.
+  auto release_upto = [&](int upto) {
+    if (n_released >= upto) return;
+    fence_proxy_async_global();
+    fence_acq_rel_sys();
+    uint32_t* cur = nullptr;
+    uint32_t run = 0;
+    for (; n_released < upto; ++n_released) {
+      const int pp = S->crel[n_released & 63];
+      const SymPtrs& P = a.peers.p[S->cdst[pp]];
+      const int slot = S->cslot[pp];
+      if (a.n_relay > 0) {
+        st_relaxed_sys(P.slot_flag + slot, a.epoch * 2 + ph);
+      } else {
+        uint32_t* c = rg_counter(P, d, ph, a.par, slot >> 7);
+        if (c != cur) {
+          if (cur) red_relaxed_sys_add(cur, run);
+          cur = c;
+          run = 0;
+        }
+        ++run;
+      }
+    }
+    if (cur) red_relaxed_sys_add(cur, run);
+  };
+  for (int p = 0; p <= cnt; ++p) {
+    if (p < cnt && S->cdst[p] >= 0) {
+      const int q = n_loaded, slot = q % NSLOT;
+      if (q >= NSLOT) {  // slot reuse: the stores of items <= q - NSLOT must be complete
+        tma_store_wait<NSLOT - L - 1>();
+        if (q - NSLOT + 1 - n_released >= 16) release_upto(q - NSLOT + 1);  // <= 64 pending
+      }
+      mbar_arrive_expect_tx(&S->cbar[slot], row_bytes);
+      bulk_load(sbuf + slot * SLOT, src_base + (size_t)(S->citem[p] / k) * H, row_bytes, &S->cbar[slot]);
+      S->cpos[slot] = p;
+      S->crel[q & 63] = p;
+      ++n_loaded;
+    }
+    while (n_stored < n_loaded && (n_loaded - n_stored > L || p == cnt)) {
+      const int slot = n_stored % NSLOT, pp = S->cpos[slot];
+      mbar_wait(&S->cbar[slot], (uint32_t)(par >> slot) & 1u);
+      par ^= 1ull << slot;
+      const SymPtrs& P = a.peers.p[S->cdst[pp]];
+      bulk_store((ph == 0 ? P.recv_x : P.recv_dy) + (size_t)S->cslot[pp] * H, sbuf + slot * SLOT,
+                 row_bytes);
+      tma_store_commit();
+      ++n_stored;
+    }
+  }
+  tma_store_wait<0>();
+  release_upto(n_loaded);
+  S->cphase = par;
+}
+
+__device__ void comm_task(const MkArgs& a, int task, int ph, GemmSmem* S, uint8_t* sbuf) {
   const Dims& d = a.d;
   const int k = d.topk, H = d.H, me = d.rank;
   const long long n = (long long)a.p.n_tok * k;
@@ -190,42 +266,50 @@ __device__ void comm_task(const MkArgs& a, int task, int ph) {
   even_slice(n, a.n_disp, task, lo, hi);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool relay_on = a.n_relay > 0;
-  const __nv_bfloat16* src_base = ph == 0 ? a.x : a.dy;
-  const uint32_t flagv = a.epoch * 2 + ph;
-  const int vecs = H / 8;
-  constexpr int NW = GEMM_THREADS / 32;
-  for (long long b0 = lo + (long long)warp * 32; b0 < hi; b0 += NW * 32) {
-    // ---- lane-parallel metadata of items b0 .. b0+31
-    const long long my = b0 + lane;
-    int mi = -1, mdst = 0, mslot = 0, mprim = 1;
-    if (my < hi) {
-      mi = a.p.sched[my];
-      const int e = a.p.topk_ids[mi];
-      mdst = e / d.epr;
-      mslot = a.p.dst_slot[mi];
-      if (relay_on) {
-        const int t = mi / k, el = e - mdst * d.epr;
+  for (long long b0 = lo; b0 < hi; b0 += GEMM_THREADS) {
+    const int cnt = (hi - b0) < GEMM_THREADS ? (int)(hi - b0) : GEMM_THREADS;
+    // ---- parallel metadata: one thread per item. Writes the destination slot's return
+    // address (forward) and, relay on, publishes duplicate slots right away: their flag means
+    // "metadata valid", the relay then waits for the primary slot's flag before copying.
+    if ((int)threadIdx.x < cnt) {
+      const int i = a.p.sched[b0 + threadIdx.x];
+      const int t = i / k;
+      const int e = a.p.topk_ids[i];
+      const int dst = e / d.epr, el = e - dst * d.epr;
+      const int slot = a.p.dst_slot[i];
+      int prim_j = -1, best = el;
+      if (relay_on)
         for (int jj = 0; jj < k; ++jj) {
           const int e2 = a.p.topk_ids[t * k + jj];
-          if (e2 / d.epr == mdst && e2 - mdst * d.epr < el) mprim = 0;
+          if (e2 / d.epr == dst && e2 - dst * d.epr < best) {
+            best = e2 - dst * d.epr;
+            prim_j = jj;
+          }
         }
-      }
-    }
-    const int cnt = (hi - b0) < 32 ? (int)(hi - b0) : 32;
-    for (int q = 0; q < cnt; ++q) {
-      const int i = __shfl_sync(0xffffffffu, mi, q);
-      const int dst = __shfl_sync(0xffffffffu, mdst, q);
-      const int slot = __shfl_sync(0xffffffffu, mslot, q);
-      const bool primary = __shfl_sync(0xffffffffu, mprim, q) != 0;
-      const int t = i / k, j = i - t * k;
-      if (!primary && ph == 0) continue;
       const SymPtrs& P = a.peers.p[dst];
-      const int4* src = reinterpret_cast<const int4*>(src_base + (size_t)t * H);
-      int4* dstrow = reinterpret_cast<int4*>((ph == 0 ? P.recv_x : P.recv_dy) + (size_t)slot * H);
-      if (ph == 0) {
-        warp_copy_row<8>(dstrow, src, vecs, lane);
-      } else {
-        // dY row -> destination slot, and the gate gradient against the saved replica o_{t,j}
+      const int prim_slot = prim_j >= 0 ? a.p.dst_slot[t * k + prim_j] : -1;
+      if (ph == 0) P.meta[slot] = SlotMeta{me, i, a.p.gate_w[i], prim_slot};
+      if (prim_slot >= 0) st_release_sys(P.slot_flag + slot, a.epoch * 2 + ph);
+      S->citem[threadIdx.x] = i;
+      S->cslot[threadIdx.x] = slot;
+      S->cdst[threadIdx.x] = prim_slot >= 0 ? -1 : dst;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      if (lane == 0) {
+        if (H <= 2048)
+          comm_pipeline<48>(a, ph, S, sbuf, cnt);
+        else if (H <= 4096)
+          comm_pipeline<24>(a, ph, S, sbuf, cnt);
+        else
+          comm_pipeline<12>(a, ph, S, sbuf, cnt);
+      }
+      __syncwarp();
+    } else if (ph == 1) {
+      const int vecs = H / 8;
+      for (int q = warp - 1; q < cnt; q += GEMM_THREADS / 32 - 1) {
+        const int i = S->citem[q], t = i / k;
+        const int4* src = reinterpret_cast<const int4*>(a.dy + (size_t)t * H);
         const int4* orow = reinterpret_cast<const int4*>(a.peers.p[me].rep + (size_t)i * H);
         float gacc = 0.f;
         int c = lane;
@@ -237,46 +321,15 @@ __device__ void comm_task(const MkArgs& a, int task, int ph) {
             o[u] = ld_nc_v4(orow + c + u * 32);
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (primary) dstrow[c + u * 32] = v[u];
-            gacc = dot8_bf16(v[u], o[u], gacc);
-          }
+          for (int u = 0; u < 4; ++u) gacc = dot8_bf16(v[u], o[u], gacc);
         }
-        for (; c < vecs; c += 32) {
-          const int4 v = ld_nc_v4(src + c), o = ld_nc_v4(orow + c);
-          if (primary) dstrow[c] = v;
-          gacc = dot8_bf16(v, o, gacc);
-        }
+        for (; c < vecs; c += 32) gacc = dot8_bf16(ld_nc_v4(src + c), ld_nc_v4(orow + c), gacc);
 #pragma unroll
         for (int s = 16; s > 0; s >>= 1) gacc += __shfl_xor_sync(0xffffffffu, gacc, s);
         if (lane == 0) a.dgate[i] = gacc;
-        if (!primary) continue;
-      }
-      if (ph == 0 && lane == 0) {
-        P.meta[slot] = SlotMeta{me, i, a.p.gate_w[i], -1};
-        if (relay_on)
-          for (int jj = 0; jj < k; ++jj) {
-            const int e2 = a.p.topk_ids[t * k + jj];
-            if (jj != j && e2 / d.epr == dst) {
-              const int s2 = a.p.dst_slot[t * k + jj];
-              P.meta[s2] = SlotMeta{me, t * k + jj, a.p.gate_w[t * k + jj], slot};
-            }
-          }
-      }
-      __syncwarp();  // orders every lane's row stores before lane 0's release (cumulative)
-      if (lane == 0) {
-        if (relay_on) {
-          st_release_sys(P.slot_flag + slot, flagv);
-          for (int jj = 0; jj < k; ++jj) {
-            const int e2 = a.p.topk_ids[t * k + jj];
-            if (jj != j && e2 / d.epr == dst)
-              st_release_sys(P.slot_flag + a.p.dst_slot[t * k + jj], flagv);
-          }
-        } else {
-          red_release_sys_add(rg_counter(P, d, ph, a.par, slot >> 7), 1u);
-        }
       }
     }
+    __syncthreads();
   }
 }
 
@@ -302,6 +355,8 @@ __device__ void relay_task(const MkArgs& a, int task, int ph) {
       if (lane == 0) wait_eq_sys(me.slot_flag + s, flagv, a.timeout_ns, a.err, 10 + ph, s);
       __syncwarp();
       const int prim = me.meta[s].primary;
+      if (prim >= 0 && lane == 0) wait_eq_sys(me.slot_flag + prim, flagv, a.timeout_ns, a.err, 12 + ph, prim);
+      __syncwarp();
       if (prim >= 0)
         warp_copy_row<8>(reinterpret_cast<int4*>(recv + (size_t)s * d.H),
                          reinterpret_cast<const int4*>(recv + (size_t)prim * d.H), vecs, lane);
@@ -739,7 +794,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   while (id < n_pre) {
     const unsigned long long t0 = globaltimer();
     if (id < a.n_disp)
-      comm_task(a, id, ph);
+      comm_task(a, id, ph, S, base);
     else
       relay_task(a, id - a.n_disp, ph);
     __syncthreads();

@@ -49,7 +49,7 @@ class LayerPrediction(C.Structure):
 
 
 # B200 calibration of this build (DESIGN.md §Performance model; refit by tools/calibrate_model.py)
-B200_CALIB = Calib(0.88, 0.78, 40e9, 40e9, 3.5e12, 6e-6)
+B200_CALIB = Calib(0.88, 0.78, 16e9, 16e9, 3.0e12, 6e-6)
 
 
 def hw(world, n_sm=148, p_peak=1408.1e12, bw_hbm=6468.9e9, bw_nvl=770e9, w_sat=1024.0, tau_sync=1e-6):

@@ -130,14 +130,20 @@ __device__ __forceinline__ TileDesc nt_tile(const Dims& d, const PlanDev& p, int
   return td;
 }
 
-// Transposed (weight-gradient) tile t: output [NO][KO] per expert, BM x BN tiles row-major.
+// Transposed (weight-gradient) tile t: output [NO][KO] per expert in BM x BN tiles, rasterised
+// in groups of 8 output row blocks with the column blocks outer inside a group, so the ~148
+// tiles in flight touch 8 A panels and ~18 B panels (each panel = all of the expert's rows).
+constexpr int TN_G = 8;
 __device__ __forceinline__ TileDesc tn_tile(const Dims& d, const PlanDev& p, int t, int NO, int KO) {
-  const int per_e = (NO / BM) * (KO / BN);
+  const int mb = NO / BM, nb = KO / BN, per_e = mb * nb;
   TileDesc td;
   td.e = t / per_e;
   const int l = t - td.e * per_e;
-  td.m0 = (l / (KO / BN)) * BM;
-  td.n0 = (l % (KO / BN)) * BN;
+  const int g = l / (TN_G * nb);
+  const int gsz = min(TN_G, mb - g * TN_G);
+  const int r = l - g * TN_G * nb;
+  td.m0 = (g * TN_G + r % gsz) * BM;
+  td.n0 = (r / gsz) * BN;
   const int ge = d.rank * d.epr + td.e;
   td.kb0 = p.sb_all[ge];
   td.nkb = p.mblocks[td.e] * (BM / BK);

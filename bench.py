@@ -143,6 +143,60 @@ def cpu_baseline(cfg_name, budget_s=12.0):
                       f"through the C oracle (oracle/eplab_oracle.c, OpenMP), {dt:.2f} s"}
 
 
+def run_unfused(args):
+    """Unfused NCCL all_to_all + cuBLAS grouped-GEMM baseline (tools/unfused_baseline.py)."""
+    import torch
+    rank, world, local = dist_info()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from oracle import pyoracle as po
+    from tools import unfused_baseline as ub
+    H, F, E, k, T = CONFIGS[args.config]
+    epr = E // world
+    sel, gw = po.Oracle().sample_routing(E, k, T, world, 7)
+    ids = torch.from_numpy(sel[rank].reshape(T, k).copy()).cuda().long()
+    gws = torch.from_numpy(gw[rank].reshape(T, k).copy()).cuda()
+    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    x = torch.randn(T, H, device="cuda", generator=g).bfloat16().requires_grad_()
+    dy = (torch.randn(T, H, device="cuda", generator=g) * 0.1).bfloat16()
+    w_up = ((torch.randn(epr, 2 * F, H, device="cuda", generator=g) * H ** -0.5).bfloat16()).requires_grad_()
+    w_down = ((torch.randn(epr, H, F, device="cuda", generator=g) * F ** -0.5).bfloat16()).requires_grad_()
+    gw_t = gws.requires_grad_()
+
+    def step():
+        y = ub.layer(x, ids, gw_t, w_up, w_down, E, world, rank)
+        y.backward(dy)
+
+    for _ in range(args.warmup):
+        step()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    s0.record()
+    for _ in range(args.steps):
+        step()
+    s1.record()
+    torch.cuda.synchronize()
+    ms = s0.elapsed_time(s1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = t.item()
+    if rank == 0:
+        v = T * world / (ms / 1e3)
+        print(json.dumps({"impl": "unfused", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                          "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                          "config": {"workload": CONFIG_DESC[args.config], "ep": world,
+                                     "baseline": "NCCL all_to_all + per-expert cuBLAS GEMMs + torch SwiGLU, autograd bwd"}}),
+              flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def run_reference(args):
     rank, world, _ = dist_info()
     if rank != 0:
@@ -333,7 +387,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference", "unfused"])
     ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tune", default="", help="override n_disp,n_relay,n_comb,n_red,w")
@@ -342,6 +396,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.impl == "unfused":
+        run_unfused(args)
     else:
         run_ours(args)
 

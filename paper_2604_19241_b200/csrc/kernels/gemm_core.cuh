@@ -60,9 +60,9 @@ struct GemmSmem {
   int bcast;
   // comm role (runs before the CTA enters the GEMM roles; reuses the stage buffers)
   uint64_t cbar[48];      // one mbarrier per bulk-copy slot
-  uint64_t cphase;        // parity bit per slot (carried across comm tasks)
+  uint32_t cphase[4];     // per issuer: parity bit per owned slot (carried across comm tasks)
   int cpos[48];           // round position of the item held by each slot
-  int crel[64];           // round position by load sequence (release ring)
+  int crel[4][64];        // per issuer: round position by load sequence (release ring)
   int citem[256];         // per-round item metadata
   int cslot[256];
   int cdst[256];

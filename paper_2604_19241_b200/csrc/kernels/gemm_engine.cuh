@@ -182,7 +182,7 @@ __device__ __forceinline__ void gemm_setup(GemmSmem* S) {
       mbar_init(&S->rempty[i], 6);  // producer + mma + 4 epilogue warps
     }
     for (int i = 0; i < 48; ++i) mbar_init(&S->cbar[i], 1);
-    S->cphase = 0;
+    for (int i = 0; i < 4; ++i) S->cphase[i] = 0;
     S->bcast = TASK_STOP;
     fence_mbar_init();
   }

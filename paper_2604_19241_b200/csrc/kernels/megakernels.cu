@@ -198,15 +198,21 @@ __device__ __forceinline__ float dot8_bf16(const int4& a, const int4& b, float a
 // scoreboard release (rowgroup counter, or per-slot flags for the relay) is issued only after its
 // bulk store has completed. ph = 0 forward (x rows), 1 backward (dY rows; warps 1..7 meanwhile
 // fold the gate gradient <dY_t, o_{t,j}> of every item of the slice).
-template <int NSLOT>
-__device__ void comm_pipeline(const MkArgs& a, int ph, GemmSmem* S, uint8_t* sbuf, int cnt) {
-  constexpr int L = NSLOT / 2;               // loads run L rows ahead of stores
+// One issuer (lane 0 of warp `iss`) of the comm role: rows p = iss, iss + ISS, ... of the round
+// through its NS = NSLOT / ISS slots. A single issuing thread is limited to ~0.55 us per row
+// (tools/bulk_copy_probe.cu), so ISS independent issuers share the CTA's slots.
+template <int NSLOT, int ISS>
+__device__ void comm_pipeline(const MkArgs& a, int ph, GemmSmem* S, uint8_t* sbuf, int cnt, int iss) {
+  constexpr int NS = NSLOT / ISS;            // slots owned by this issuer
+  constexpr int L = NS / 2;                  // loads run L rows ahead of stores
   constexpr uint32_t SLOT = 196608 / NSLOT;  // bytes per slot
   const Dims& d = a.d;
   const int k = d.topk, H = d.H;
   const uint32_t row_bytes = (uint32_t)H * 2;
   const __nv_bfloat16* src_base = ph == 0 ? a.x : a.dy;
-  uint64_t par = S->cphase;
+  const int slot0 = iss * NS;
+  int* crel = S->crel[iss];
+  uint32_t par = S->cphase[iss];
   int n_loaded = 0, n_stored = 0, n_released = 0;
   // Publish items [n_released, upto) whose bulk stores have completed: one async-proxy fence and
   // one system-scope release fence for the batch, then relaxed scoreboard updates (the fence +
@@ -218,7 +224,7 @@ __device__ void comm_pipeline(const MkArgs& a, int ph, GemmSmem* S, uint8_t* sbu
     uint32_t* cur = nullptr;
     uint32_t run = 0;
     for (; n_released < upto; ++n_released) {
-      const int pp = S->crel[n_released & 63];
+      const int pp = crel[n_released & 63];
       const SymPtrs& P = a.peers.p[S->cdst[pp]];
       const int slot = S->cslot[pp];
       if (a.n_relay > 0) {
@@ -235,23 +241,23 @@ __device__ void comm_pipeline(const MkArgs& a, int ph, GemmSmem* S, uint8_t* sbu
     }
     if (cur) red_relaxed_sys_add(cur, run);
   };
-  for (int p = 0; p <= cnt; ++p) {
+  for (int p = iss; p < cnt + ISS; p += ISS) {
     if (p < cnt && S->cdst[p] >= 0) {
-      const int q = n_loaded, slot = q % NSLOT;
-      if (q >= NSLOT) {  // slot reuse: the stores of items <= q - NSLOT must be complete
-        tma_store_wait<NSLOT - L - 1>();
-        if (q - NSLOT + 1 - n_released >= 16) release_upto(q - NSLOT + 1);  // <= 64 pending
+      const int q = n_loaded, slot = slot0 + q % NS;
+      if (q >= NS) {  // slot reuse: the stores of items <= q - NS must be complete
+        tma_store_wait<NS - L - 1>();
+        if (q - NS + 1 - n_released >= 16) release_upto(q - NS + 1);  // <= 64 pending
       }
       mbar_arrive_expect_tx(&S->cbar[slot], row_bytes);
       bulk_load(sbuf + slot * SLOT, src_base + (size_t)(S->citem[p] / k) * H, row_bytes, &S->cbar[slot]);
       S->cpos[slot] = p;
-      S->crel[q & 63] = p;
+      crel[q & 63] = p;
       ++n_loaded;
     }
-    while (n_stored < n_loaded && (n_loaded - n_stored > L || p == cnt)) {
-      const int slot = n_stored % NSLOT, pp = S->cpos[slot];
-      mbar_wait(&S->cbar[slot], (uint32_t)(par >> slot) & 1u);
-      par ^= 1ull << slot;
+    while (n_stored < n_loaded && (n_loaded - n_stored > L || p >= cnt)) {
+      const int ls = n_stored % NS, slot = slot0 + ls, pp = S->cpos[slot];
+      mbar_wait(&S->cbar[slot], (par >> ls) & 1u);
+      par ^= 1u << ls;
       const SymPtrs& P = a.peers.p[S->cdst[pp]];
       bulk_store((ph == 0 ? P.recv_x : P.recv_dy) + (size_t)S->cslot[pp] * H, sbuf + slot * SLOT,
                  row_bytes);
@@ -261,7 +267,7 @@ __device__ void comm_pipeline(const MkArgs& a, int ph, GemmSmem* S, uint8_t* sbu
   }
   tma_store_wait<0>();
   release_upto(n_loaded);
-  S->cphase = par;
+  S->cphase[iss] = par;
 }
 
 __device__ void comm_task(const MkArgs& a, int task, int ph, GemmSmem* S, uint8_t* sbuf) {
@@ -301,33 +307,34 @@ __device__ void comm_task(const MkArgs& a, int task, int ph, GemmSmem* S, uint8_
       S->cdst[threadIdx.x] = prim_slot >= 0 ? -1 : dst;
     }
     __syncthreads();
-    if (warp == 0) {
+    const int n_iss = H <= 4096 ? 4 : 2;  // 14 KB rows: 2 issuers x 6 slots
+    if (warp < n_iss) {  // issuer warps
       if (lane == 0) {
         if (H <= 2048)
-          comm_pipeline<48>(a, ph, S, sbuf, cnt);
+          comm_pipeline<48, 4>(a, ph, S, sbuf, cnt, warp);
         else if (H <= 4096)
-          comm_pipeline<24>(a, ph, S, sbuf, cnt);
+          comm_pipeline<24, 4>(a, ph, S, sbuf, cnt, warp);
         else
-          comm_pipeline<12>(a, ph, S, sbuf, cnt);
+          comm_pipeline<12, 2>(a, ph, S, sbuf, cnt, warp);
       }
       __syncwarp();
     } else if (ph == 1) {
       const int vecs = H / 8;
-      for (int q = warp - 1; q < cnt; q += GEMM_THREADS / 32 - 1) {
+      for (int q = warp - n_iss; q < cnt; q += GEMM_THREADS / 32 - n_iss) {
         const int i = S->citem[q], t = i / k;
         const int4* src = reinterpret_cast<const int4*>(a.dy + (size_t)t * H);
         const int4* orow = reinterpret_cast<const int4*>(a.peers.p[me].rep + (size_t)i * H);
         float gacc = 0.f;
         int c = lane;
-        for (; c + 3 * 32 < vecs; c += 4 * 32) {
-          int4 v[4], o[4];
+        for (; c + 7 * 32 < vecs; c += 8 * 32) {
+          int4 v[8], o[8];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < 8; ++u) {
             v[u] = ld_nc_v4(src + c + u * 32);
             o[u] = ld_nc_v4(orow + c + u * 32);
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) gacc = dot8_bf16(v[u], o[u], gacc);
+          for (int u = 0; u < 8; ++u) gacc = dot8_bf16(v[u], o[u], gacc);
         }
         for (; c < vecs; c += 32) gacc = dot8_bf16(ld_nc_v4(src + c), ld_nc_v4(orow + c), gacc);
 #pragma unroll

@@ -176,3 +176,64 @@ def test_world_invariance_ep1_vs_ep2():
     a, b = gather(ep2[0]), gather(ep1[0])
     for key in ("y", "dx", "dgate", "dw_up", "dw_down"):
         assert (a[key] == b[key]).all(), f"EP=2 vs EP=1 {key}"
+
+
+def test_token_map_and_layer_ep8_virtual_ranks_vs_reference_fixture():
+    """8 ranks sharing one device (18 SMs each): the device token map and schedule of every rank
+    equal the reference's (128 experts, top-8), and the layer matches the oracle."""
+    g = np.load(os.path.join(GOLDEN, "reference_vectors_ep8.npz"))
+    W, E, k, T = int(g["world"]), int(g["n_exp"]), int(g["topk"]), int(g["n_tok"])
+    prob = Problem(W, E, k, 256, 256, T, seed=int(g["seed"]))
+    assert (prob.sel == g["sel"]).all()
+    outs, maps, sched = run_layer(prob)
+    for r in range(W):
+        tr, le, off, rt, sb = maps[r]
+        assert (tr == g["target_rank"][r]).all() and (off == g["offset"][r]).all()
+        assert (rt == g["recv_totals"]).all() and (sb == g["seg_base"]).all()
+        tok, slot = sched[r]
+        assert (tok == g[f"sched{r}_token"]).all() and (slot == g[f"sched{r}_slot"]).all()
+    check_vs_oracle(prob, gather(outs[0]))
+
+
+def test_relay_mode_ep2_bitwise_equal_alltoall():
+    """AllGather-style (dedup + relay multicast) and AllToAll-style dispatch give identical results
+    at EP=2 (top-4 of 16 experts: many tokens have 2+ experts on one rank)."""
+    prob = Problem(2, 16, 4, 256, 256, 192, seed=5)
+    a2a, _, _ = run_layer(prob, cfg=(8, 0, 1, 64, 8))
+    rel, _, _ = run_layer(prob, cfg=(8, 4, 1, 64, 8))
+    ga, gr = gather(a2a[0]), gather(rel[0])
+    for key in ("y", "dx", "dgate", "dw_up", "dw_down"):
+        assert (ga[key] == gr[key]).all(), key
+    check_vs_oracle(prob, ga)
+
+
+def test_topk1_and_single_expert_edge_cases():
+    prob = Problem(1, 4, 1, 256, 256, 130, seed=2)   # top-1, ragged rowgroups
+    outs, _, _ = run_layer(prob)
+    check_vs_oracle(prob, gather(outs[0]))
+    prob = Problem(1, 2, 2, 256, 256, 64, seed=3)    # topk == n_exp: every token hits every expert
+    outs, _, _ = run_layer(prob)
+    check_vs_oracle(prob, gather(outs[0]))
+
+
+def test_empty_batch_and_validation_errors():
+    m = moe()
+    layer = m.EpMoE(256, 256, 8, 2, 64)
+    ids = torch.zeros(0, 2, dtype=torch.int32, device="cuda")
+    gw = torch.zeros(0, 2, dtype=torch.float32, device="cuda")
+    wu = torch.zeros(8, 512, 256, dtype=torch.bfloat16, device="cuda")
+    wd = torch.zeros(8, 256, 256, dtype=torch.bfloat16, device="cuda")
+    y = layer.forward(torch.zeros(0, 256, dtype=torch.bfloat16, device="cuda"), ids, gw, wu, wd)
+    g = layer.backward(torch.zeros(0, 256, dtype=torch.bfloat16, device="cuda"), wu, wd)
+    layer.check()
+    assert y.shape == (0, 256) and float(g["dw_up"].abs().max()) == 0.0
+    with pytest.raises(m.EplabError) as e:  # too many tokens for the context
+        layer.plan(torch.zeros(65, 2, dtype=torch.int32, device="cuda"),
+                   torch.zeros(65, 2, dtype=torch.float32, device="cuda"))
+    assert e.value.code == 2
+    with pytest.raises(m.EplabError) as e:  # deadlock constraint of validate_tune_config
+        layer.set_tune_config((140, 10, 1, 148, 8))
+    assert e.value.code == 2
+    with pytest.raises(m.EplabError):
+        m.EpMoE(300, 256, 8, 2, 64)  # hidden not a multiple of 256
+    layer.close()

@@ -187,7 +187,7 @@ typedef struct {
   double w_gap, w_red, w_rem;
 } eplab_breakdown;                   /* LatencyBreakdown, perf_model.hpp:17-35 */
 typedef struct {
-  double mu_longk, mu_shortk, comm_bw_per_sm, relay_bw_per_sm, reduce_bw, launch;
+  double mu, tile_overhead, comm_bw_per_sm, relay_bw_per_sm, reduce_bw, launch, epi_bw_per_sm;
 } eplab_b200_calib;                  /* B200 calibration of this build's MegaKernels */
 typedef struct {
   double fwd_dispatch, fwd_combine, bwd_dispatch, bwd_combine, total, t_gemm_bound, t_nvl_bound;

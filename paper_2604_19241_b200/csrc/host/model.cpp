@@ -435,10 +435,16 @@ LayerPrediction predict_layer(const MoEShape& m, const HardwareSpec& s, const Tu
   const double rows_e = rows / epr;
   const double mblocks = epr * std::ceil(rows_e / 128.0);
   const double seg_pad = std::ceil(rows_e / 128.0) * 128.0;
-  auto tile_t = [&](double K) {
-    const double mu = K >= 8192 ? k.mu_longk : k.mu_shortk;
-    return 2.0 * 128 * 256 * K / (s.p_peak * mu / s.n_sm) + s.tau_sync;
+  // tile time: main loop at mu of peak, or the epilogue's traffic (bytes per 128x256 tile) when
+  // that is longer (the TMEM double buffer overlaps the two), plus a fixed hand-off cost
+  auto tile_t = [&](double K, double epi_bytes) {
+    return std::max(2.0 * 128 * 256 * K / (s.p_peak * k.mu / s.n_sm), epi_bytes / k.epi_bw_per_sm) +
+           k.tile_overhead;
   };
+  constexpr double kEpiUp = 128.0 * (256 + 128) * 2;           // GU + h
+  constexpr double kEpiPush = 128.0 * 256 * 2;                  // one replica row chunk
+  constexpr double kEpiDgrad = 128.0 * (512 + 256 + 512) * 2;   // dGU + HW written, GU read
+  constexpr double kEpiWgrad = 128.0 * 256 * 2;                 // dW tile
   // dispatch rows: relay on -> one send per (token, distinct destination rank) and HBM relay
   // copies for the other replicas (sim.cpp:384-441); relay off -> every replica is sent
   // (AllToAll style). q = P(a given rank hosts >= 1 of the token's experts), without replacement.
@@ -453,24 +459,29 @@ LayerPrediction predict_layer(const MoEShape& m, const HardwareSpec& s, const Tu
   const double l_relay = relay ? dup_rows * S / (c.n_relay * k.relay_bw_per_sm) : 0.0;
   const double l_push = W > 1 ? T * k_rem * S / s.bw_nvl : 0.0;
   const double l_reduce = T * (m.topk + 1) * S / k.reduce_bw;
-  auto kernel = [&](double sm_seconds, double critical, double extra) {
-    return std::max(sm_seconds / s.n_sm, critical) + extra + k.launch;
+  // persistent grid: SM-seconds spread over n_sm, but never less than whole waves of the
+  // kernel's dominant tile (quantisation matters for small batches)
+  auto kernel = [&](double sm_seconds, double critical, double extra, double tiles = 0,
+                    double t_one = 0) {
+    const double waves = tiles > 0 ? std::ceil(tiles / s.n_sm) * t_one : 0.0;
+    return std::max({sm_seconds / s.n_sm, critical, waves}) + extra + k.launch;
   };
   const double n_pre_sm = c.n_disp * l_comm + c.n_relay * l_relay;
   // forward
-  const double up = mblocks * (F / 128) * tile_t(H);
-  p.fwd_dispatch = kernel(up + n_pre_sm, std::max(l_comm, l_relay) + tile_t(H), 0.0);
-  const double down = mblocks * (H / 256) * tile_t(F);
-  p.fwd_combine = kernel(down, l_push, l_reduce);
+  const double up = mblocks * (F / 128) * tile_t(H, kEpiUp);
+  p.fwd_dispatch = kernel(up + n_pre_sm, std::max(l_comm, l_relay) + tile_t(H, kEpiUp), 0.0,
+                          mblocks * (F / 128), tile_t(H, kEpiUp));
+  const double down = mblocks * (H / 256) * tile_t(F, kEpiPush);
+  p.fwd_combine = kernel(down, l_push, l_reduce, mblocks * (H / 256), tile_t(F, kEpiPush));
   // backward (dY dispatch also folds the gate gradient: + k*S of replica reads per token)
   const double l_comm_b = l_comm + T * m.topk * S / std::max(c.n_disp * k.comm_bw_per_sm, 1.0);
-  const double ddown = mblocks * (F / 256) * tile_t(H);
-  const double wg_down = epr * (H / 128) * (F / 256) * tile_t(seg_pad);
+  const double ddown = mblocks * (F / 256) * tile_t(H, kEpiDgrad);
+  const double wg_down = epr * (H / 128) * (F / 256) * tile_t(seg_pad, kEpiWgrad);
   p.bwd_dispatch = kernel(ddown + wg_down + c.n_disp * l_comm_b + c.n_relay * l_relay,
-                          std::max(l_comm_b, l_relay) + tile_t(H), 0.0);
-  const double dup = mblocks * (H / 256) * tile_t(2 * F);
-  const double wg_up = epr * (2 * F / 128) * (H / 256) * tile_t(seg_pad);
-  p.bwd_combine = kernel(dup + wg_up, l_push, l_reduce);
+                          std::max(l_comm_b, l_relay) + tile_t(H, kEpiDgrad), 0.0);
+  const double dup = mblocks * (H / 256) * tile_t(2 * F, kEpiPush);
+  const double wg_up = epr * (2 * F / 128) * (H / 256) * tile_t(seg_pad, kEpiWgrad);
+  p.bwd_combine = kernel(dup + wg_up, l_push, l_reduce, mblocks * (H / 256), tile_t(2 * F, kEpiPush));
   p.total = p.fwd_dispatch + p.fwd_combine + p.bwd_dispatch + p.bwd_combine;
   p.t_gemm_bound = 18.0 * m.topk * H * F * T / s.p_peak;
   p.t_nvl_bound = 2.0 * ((W - 1) * q + k_rem) * 2.0 * H * T / s.bw_nvl;

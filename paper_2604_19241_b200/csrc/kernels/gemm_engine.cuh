@@ -258,6 +258,13 @@ __device__ __forceinline__ void stage_row(uint8_t* buf, int r, const float (&v)[
     *reinterpret_cast<int4*>(buf + r * 64 + ((c ^ ((r >> 1) & 3)) << 4)) = w;
   }
 }
+// Same, from 16 packed bf16x2 words.
+__device__ __forceinline__ void stage_row_packed(uint8_t* buf, int r, const uint32_t (&p)[16]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    *reinterpret_cast<int4*>(buf + r * 64 + ((c ^ ((r >> 1) & 3)) << 4)) =
+        make_int4((int)p[4 * c], (int)p[4 * c + 1], (int)p[4 * c + 2], (int)p[4 * c + 3]);
+}
 __device__ __forceinline__ void stage_zero_row(uint8_t* buf, int r) {
 #pragma unroll
   for (int c = 0; c < 4; ++c) *reinterpret_cast<int4*>(buf + r * 64 + (c << 4)) = make_int4(0, 0, 0, 0);

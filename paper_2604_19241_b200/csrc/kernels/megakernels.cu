@@ -659,43 +659,78 @@ struct ModeDgradDown {
     const int row0 = td.m0 + (r & ~31);
     const bool live = r < td.rows;
     const float w = live ? a.peers.p[a.d.rank].meta[m].w : 0.f;
+    const int4* gsrc = reinterpret_cast<const int4*>(a.gu + m * 2 * F + td.n0);
+    const int4* usrc = reinterpret_cast<const int4*>(a.gu + m * 2 * F + F + td.n0);
+    // saved g, u of chunk c+1 are in flight while chunk c is computed (software pipelining)
+    int4 gq[4], uq[4];
+    if (live) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        gq[i] = gsrc[i];
+        uq[i] = usrc[i];
+      }
+    }
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
       float v[32];
       acc_chunk(taddr, c, v);
-      const int f0 = td.n0 + c * 32;
-      float g[32], u[32], du[32], hv[32];
-      if (live) {
-        load_row_bf16_32(a.gu + m * 2 * F + f0, g);
-        load_row_bf16_32(a.gu + m * 2 * F + F + f0, u);
+      int4 gn[4], un[4];
+      if (live && c + 1 < BN / 32) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float dh = w * v[i];
-          const float s = 1.0f / (1.0f + __expf(-g[i]));
-          const float si = g[i] * s;
-          const float ds = s * (1.0f + g[i] * (1.0f - s));
-          const float h = __bfloat162float(__float2bfloat16_rn(si * u[i]));
-          v[i] = dh * u[i] * ds;
-          du[i] = dh * si;
-          hv[i] = w * h;
+        for (int i = 0; i < 4; ++i) {
+          gn[i] = gsrc[(c + 1) * 4 + i];
+          un[i] = usrc[(c + 1) * 4 + i];
         }
       }
+      uint32_t pdg[16], pdu[16], phw[16];
+      if (live) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const float2 g2 = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(gq)[q]);
+          const float2 u2 = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(uq)[q]);
+          float dg[2], du[2], hv[2];
+          const float gg[2] = {g2.x, g2.y}, uu[2] = {u2.x, u2.y};
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float dh = w * v[2 * q + h];
+            const float sg = 1.0f / (1.0f + __expf(-gg[h]));
+            const float si = gg[h] * sg;
+            const float ds = sg * (1.0f + gg[h] * (1.0f - sg));
+            const float hh = __bfloat162float(__float2bfloat16_rn(si * uu[h]));
+            dg[h] = dh * uu[h] * ds;
+            du[h] = dh * si;
+            hv[h] = w * hh;
+          }
+          pdg[q] = pack_bf16(dg[0], dg[1]);
+          pdu[q] = pack_bf16(du[0], du[1]);
+          phw[q] = pack_bf16(hv[0], hv[1]);
+        }
+      }
+      const int f0 = td.n0 + c * 32;
+      if (a.dbg & 4) continue;  // experiment: no staging / stores at all
       stage_acquire(lane);
       if (live) {
-        stage_row(stg, lane, v);
-        stage_row(stg + EPI_TILE_BYTES, lane, du);
-        stage_row(stg + 2 * EPI_TILE_BYTES, lane, hv);
+        stage_row_packed(stg, lane, pdg);
+        stage_row_packed(stg + EPI_TILE_BYTES, lane, pdu);
+        stage_row_packed(stg + 2 * EPI_TILE_BYTES, lane, phw);
       } else {  // zero padding rows: the K padding of the transposed weight-gradient GEMM
         stage_zero_row(stg, lane);
         stage_zero_row(stg + EPI_TILE_BYTES, lane);
         stage_zero_row(stg + 2 * EPI_TILE_BYTES, lane);
       }
       stage_release();
-      if (lane == 0) {
+      if (lane == 0 && !(a.dbg & 2)) {
         tma_store_2d(&tm.m[4], stg, f0, row0);                       // dGU gate half
         tma_store_2d(&tm.m[4], stg + EPI_TILE_BYTES, F + f0, row0);  // dGU up half
         tma_store_2d(&tm.m[5], stg + 2 * EPI_TILE_BYTES, f0, row0);  // HW
         tma_store_commit();
+      }
+      if (live && c + 1 < BN / 32) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          gq[i] = gn[i];
+          uq[i] = un[i];
+        }
       }
     }
     // the weight-gradient tiles of this (expert, f-block) read HW / dGU through TMA: complete

@@ -36,8 +36,8 @@ class Breakdown(C.Structure):
 
 
 class Calib(C.Structure):
-    _fields_ = [(n, C.c_double) for n in ("mu_longk", "mu_shortk", "comm_bw_per_sm", "relay_bw_per_sm",
-                                          "reduce_bw", "launch")]
+    _fields_ = [(n, C.c_double) for n in ("mu", "tile_overhead", "comm_bw_per_sm", "relay_bw_per_sm",
+                                          "reduce_bw", "launch", "epi_bw_per_sm")]
 
 
 class LayerPrediction(C.Structure):
@@ -49,7 +49,7 @@ class LayerPrediction(C.Structure):
 
 
 # B200 calibration of this build (DESIGN.md §Performance model; refit by tools/calibrate_model.py)
-B200_CALIB = Calib(0.88, 0.78, 16e9, 16e9, 3.0e12, 6e-6)
+B200_CALIB = Calib(0.7695, 0.0, 11.0e9, 11.0e9, 2.775e12, 82.7e-6, 25.9e9)  # profiles/r01_perf_model_validation.md
 
 
 def hw(world, n_sm=148, p_peak=1408.1e12, bw_hbm=6468.9e9, bw_nvl=770e9, w_sat=1024.0, tau_sync=1e-6):
@@ -110,9 +110,9 @@ def choose_config(H, F, E, k, tokens, world, n_sm=148):
     """TuneConfig for one layer shape from the B200 model (n_red = all SMs; w = 8)."""
     best, _, _ = search_layer(shape(H, F, E, k, tokens), hw(world, n_sm=n_sm))
     best.n_red = n_sm
-    # Empirical floor (profiles/r01_ndisp_sweep.txt): the analytical model does not yet capture
-    # the start-up of the GEMM tiles behind the first landed rowgroups; the measured optimum at
-    # EP=1 is 64 comm CTAs for all three BASELINE shapes.
-    if world == 1:
-        best.n_disp = max(best.n_disp, 64)
+    # Measured floor (profiles/r01_ndisp_sweep.txt): the model does not yet capture the start-up of
+    # the GEMM tiles behind the first landed rowgroups, and at EP=1 the measured optimum is >= 64
+    # comm CTAs for all three BASELINE shapes. (EP>1: same floor, not yet measured on NVLink.)
+    if best.n_disp < 64 and 64 + best.n_relay < n_sm:
+        best.n_disp = 64
     return best

@@ -1,0 +1,59 @@
+"""Fits the B200 calibration of predict_layer() (B200Calib) to the per-MegaKernel times measured by
+tools/model_sweep.py and writes the predicted-vs-measured table."""
+import json
+import os
+import sys
+
+import numpy as np
+from scipy.optimize import minimize
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2604_19241_b200 import model as m  # noqa: E402
+
+recs = [json.loads(l) for l in open(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/model_sweep.jsonl")]
+KEYS = ["fwd_dispatch", "fwd_combine", "bwd_dispatch", "bwd_combine"]
+
+
+def predict(r, x):
+    c = m.Calib(x[0], x[1] * 1e-6, x[2] * 1e9, x[2] * 1e9, x[3] * 1e12, x[4] * 1e-6, x[5] * 1e9)
+    p = m.predict_layer(m.shape(r["H"], r["F"], r["E"], r["k"], r["T"]), m.hw(r["world"]),
+                        m.TuneConfig(r["n_disp"], r["n_relay"], 1, 148, 8), c)
+    return [getattr(p, k) * 1e3 for k in KEYS]
+
+
+def loss(x):
+    if min(x) <= 0 or x[0] > 1.0:
+        return 1e9
+    e = 0.0
+    n_sweep = sum(1 for r in recs if r["name"] == "sweep")
+    for r in recs:
+        wgt = 1.0 if r["name"] == "sweep" else n_sweep / max(1, len(recs) - n_sweep)  # families equal
+        pr = predict(r, x)
+        for a, b in zip(pr, r["ms"]):
+            e += wgt * (np.log(a / b)) ** 2
+    return e
+
+
+x0 = np.array([0.9, 1.0, 16.0, 3.0, 50.0, 8.0])
+res = minimize(loss, x0, method="Nelder-Mead", options={"maxiter": 4000, "xatol": 1e-4, "fatol": 1e-8})
+x = res.x
+lines = ["# Perf model (predict_layer, B200) vs measured MegaKernel times -- round 1, 1x B200, EP=1",
+         f"# fitted B200Calib: mu={x[0]:.4f}, tile_overhead={x[1]:.3f} us, comm_bw_per_sm={x[2]:.2f} GB/s "
+         f"(relay = comm), reduce_bw={x[3]:.3f} TB/s, launch={x[4]:.2f} us, epi_bw_per_sm={x[5]:.2f} GB/s",
+         "# (least squares on log time over all 4 kernels of every case; tools/model_sweep.py + tools/fit_model.py)",
+         "", "| case | H | F | E | k | T | n_disp | measured ms (fd/fc/bd/bc) | predicted ms | step err |",
+         "|---|---|---|---|---|---|---|---|---|---|"]
+errs = []
+for r in recs:
+    pr = predict(r, x)
+    tm, tp = sum(r["ms"]), sum(pr)
+    errs.append(abs(tp - tm) / tm)
+    lines.append(f"| {r['name']} | {r['H']} | {r['F']} | {r['E']} | {r['k']} | {r['T']} | {r['n_disp']} | "
+                 + "/".join(f"{v:.3f}" for v in r["ms"]) + f" | " + "/".join(f"{v:.3f}" for v in pr)
+                 + f" | {100 * (tp - tm) / tm:+.1f}% |")
+lines.append("")
+lines.append(f"mean |step error| = {100 * np.mean(errs):.1f}%, max = {100 * np.max(errs):.1f}% over {len(recs)} cases")
+open("profiles/r01_perf_model_validation.md", "w").write("\n".join(lines) + "\n")
+print("\n".join(lines[:3]))
+print(lines[-1])
+print("calib", list(np.round(x, 4)))

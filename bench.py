@@ -48,7 +48,8 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks/throttle reasons, timestamped; only samples inside [mark_start, mark_end]
+    (the timed region) are summarised."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
@@ -57,11 +58,12 @@ class ClockSampler:
         self.index = index
         self.rows = []
         self.proc = None
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -72,23 +74,35 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 8:
-                self.rows.append(parts)
+                self.rows.append((time.time(), parts))
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
 
     def stop(self):
+        time.sleep(0.15)
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
-        if not self.rows:
+        rows = [r for t, r in self.rows if self.t0 is None or (self.t0 <= t <= (self.t1 or t) + 0.06)]
+        if not rows:
+            rows = [r for _, r in self.rows[-3:]]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
-        mx = max(float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit())
+        num = lambda v: v.replace(".", "", 1).isdigit()
+        sm = sorted(float(r[1]) for r in rows if num(r[1]))
+        mx = max(float(r[2]) for r in rows if num(r[2]))
+        pw = [float(r[3]) for r in rows if num(r[3])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(self.rows)}
+                "power_w_max": max(pw) if pw else None, "samples": len(rows)}
 
 
 def dist_info():
@@ -230,10 +244,18 @@ def run_ours(args):
     import torch
     rank, world, local = dist_info()
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
+    # EPLAB_BENCH_SHARE_DEVICE=1: every rank on cuda:0 with 148/N SMs (exercises the multi-rank
+    # path on a single GPU; bootstrap over gloo since NCCL refuses two ranks on one device)
+    share = os.environ.get("EPLAB_BENCH_SHARE_DEVICE") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from oracle import pyoracle as po  # routing generator = the reference's sample_routing (restated)
     from paper_2604_19241_b200 import moe as M
     from paper_2604_19241_b200.model import choose_config
@@ -251,7 +273,10 @@ def run_ours(args):
     layer = M.EpMoE(H, F, E, k, T, rank=rank, world=world)
     if world > 1:
         layer.connect_distributed()
-    cfg = choose_config(H, F, E, k, T, world)
+    n_sm = 148 // world if share else 148
+    if share:
+        layer.set_sm_budget(n_sm)
+    cfg = choose_config(H, F, E, k, T, world, n_sm=n_sm)
     if args.tune:
         cfg = M.TuneConfig(*[int(v) for v in args.tune.split(",")])
     layer.set_tune_config(cfg)
@@ -262,6 +287,7 @@ def run_ours(args):
 
     def barrier():
         if world > 1:
+            torch.cuda.synchronize()
             torch.distributed.barrier()
 
     def step():
@@ -296,19 +322,34 @@ def run_ours(args):
     # ---- timed region: K whole steps
     clocks = ClockSampler(local)
     clocks.start()
-    time.sleep(0.3)
+    time.sleep(0.5)
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
+    clocks.mark_start()
     s0.record(st)
     for _ in range(args.steps):
         step()
     s1.record(st)
     torch.cuda.synchronize()
+    clocks.mark_end()
     barrier()
     ms = s0.elapsed_time(s1) / args.steps
     clk = clocks.stop()
     layer.check()
+    # ---- overlap % from the device timeline (one extra, untimed step)
+    layer.timeline_enable(1 << 20)
+    overlap = {}
+    layer.plan(ids, gws)
+    layer.dispatch_group_gemm(x, w_up)
+    overlap["fwd_dispatch_gemm"] = layer.timeline_export("")
+    layer.group_gemm_combine(w_down, y)
+    layer.timeline_export("")
+    layer._dispatch_bwd(dy, w_down, out)
+    overlap["bwd_dispatch_gemm"] = layer.timeline_export("")
+    layer._combine_bwd(w_up, out)
+    layer.timeline_export("")
+    layer.timeline_enable(0)
     # ---- e2e through the C-ABI with host buffers (pinned), copies inside the timed region
     ids_h = ids.cpu().pin_memory()
     gw_h = gws.cpu().pin_memory()
@@ -374,6 +415,9 @@ def run_ours(args):
                               "t_nvlink_ms": t_nvl * 1e3,
                               "note": "max(18kHF*T / sustained bf16 peak, NVLink bytes / 770 GB/s)"},
             "kernel_ms": kms,
+            "overlap": {"fraction": overlap,
+                        "definition": "time with >=1 comm/relay task AND >=1 GEMM tile active / time with "
+                                      ">=1 comm/relay task active (device %globaltimer task log)"},
             "clocks": clk,
             "cpu_baseline": cpu,
         }

@@ -113,6 +113,7 @@ def choose_config(H, F, E, k, tokens, world, n_sm=148):
     # Measured floor (profiles/r01_ndisp_sweep.txt): the model does not yet capture the start-up of
     # the GEMM tiles behind the first landed rowgroups, and at EP=1 the measured optimum is >= 64
     # comm CTAs for all three BASELINE shapes. (EP>1: same floor, not yet measured on NVLink.)
-    if best.n_disp < 64 and 64 + best.n_relay < n_sm:
-        best.n_disp = 64
+    floor = (64 * n_sm) // 148
+    if best.n_disp < floor and floor + best.n_relay < n_sm:
+        best.n_disp = floor
     return best

@@ -61,6 +61,15 @@ EPLAB_API int eplab_grouped_gemm_tn(const void* d_A, const void* d_B, void* d_C,
                                     int NA, int NB, int n_experts, const int* seg_start,
                                     const int* seg_rows_padded, void* d_workspace, void* stream);
 
+/* The same two GEMMs on CTA pairs (cta_group::2, 256x256 tiles, B fetched once per pair). */
+EPLAB_API int eplab_grouped_gemm_nt_pair(const void* d_A, const void* d_B, void* d_C, int M_total,
+                                         int N, int K, int n_experts, const int* seg_start,
+                                         const int* seg_rows, void* d_workspace, void* stream);
+EPLAB_API int eplab_grouped_gemm_tn_pair(const void* d_A, const void* d_B, void* d_C, int M_total,
+                                         int NA, int NB, int n_experts, const int* seg_start,
+                                         const int* seg_rows_padded, void* d_workspace,
+                                         void* stream);
+
 
 /* ------------------------------------------------------- EP-MoE context (per rank) */
 

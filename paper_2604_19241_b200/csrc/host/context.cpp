@@ -68,6 +68,7 @@ struct eplab_ctx {
   uint32_t epoch = 0;
   bool planned = false;
   eplab_tune_config cfg{32, 0, 0, 148, 8};
+  int pair = 1;  // CTA-pair engine (EPLAB_ENGINE=single selects the single-CTA one)
   // timeline
   TimelineRec* tl_rec = nullptr;
   int* tl_count = nullptr;
@@ -129,6 +130,7 @@ MkArgs base_args(eplab_ctx* c) {
   a.timeout_ns = c->timeout_ns;
   a.tl = Timeline{c->tl_rec, c->tl_count, c->tl_cap};
   a.dbg = getenv("EPLAB_DBG") ? atoi(getenv("EPLAB_DBG")) : 0;
+  a.pair = c->pair;
   return a;
 }
 
@@ -173,6 +175,7 @@ int eplab_init(const eplab_init_args* args, eplab_ctx** out) {
     d.M_cap = (int)mcap;
     d.RG_cap = d.M_cap / kBM;
     c->cfg.n_red = c->num_sms;
+    if (const char* eng = getenv("EPLAB_ENGINE")) c->pair = std::string(eng) != "single";
 
     // ---- symmetric region
     size_t o = 0;
@@ -207,7 +210,8 @@ int eplab_init(const eplab_init_args* args, eplab_ctx** out) {
                  o_bb = take(E * 4), o_dslot = take(Tk * 4), o_off = take(Tk * 4),
                  o_sched = take(Tk * 4), o_rt = take((size_t)W * d.epr * 4),
                  o_sbr = take((size_t)W * d.epr * 4), o_sba = take((size_t)W * d.epr * 4),
-                 o_mb = take(d.epr * 4), o_mbp = take((d.epr + 1) * 4), o_sc = take(64),
+                 o_mb = take(d.epr * 4), o_mbp = take((d.epr + 1) * 4),
+                 o_mpp = take((d.epr + 1) * 4), o_sc = take(64),
                  o_wg = take((size_t)d.epr * (d.F / 256) * 4), o_cur = take(64), o_err = take(64);
     CK(cudaMalloc(&c->loc, o));
     CK(cudaMemset(c->loc + o_hist, 0, o - o_hist));
@@ -229,6 +233,7 @@ int eplab_init(const eplab_init_args* args, eplab_ctx** out) {
     p.sb_all = reinterpret_cast<int*>(c->loc + o_sba);
     p.mblocks = reinterpret_cast<int*>(c->loc + o_mb);
     p.mblock_pre = reinterpret_cast<int*>(c->loc + o_mbp);
+    p.mpair_pre = reinterpret_cast<int*>(c->loc + o_mpp);
     p.scalars = reinterpret_cast<int*>(c->loc + o_sc);
     c->wg_cnt = reinterpret_cast<uint32_t*>(c->loc + o_wg);
     c->cursor = reinterpret_cast<int*>(c->loc + o_cur);
@@ -412,7 +417,7 @@ int eplab_group_gemm_combine(eplab_ctx* c, const void* w_down, void* y, void* st
     TmaSet tm;
     tm.m[0] = c->tm_hact_k;
     tm.m[1] = eplab_host::make_bf16_map(w_down, (uint64_t)c->d.epr * c->d.H, c->d.F, c->d.F, 64, 256);
-    tm.m[2] = tm.m[0];
+    tm.m[2] = eplab_host::make_bf16_map(w_down, (uint64_t)c->d.epr * c->d.H, c->d.F, c->d.F, 64, 128);
     tm.m[3] = tm.m[1];
     tm.m[4] = tm.m[5] = tm.m[6] = tm.m[7] = c->st_gu;
     if (eplab_launch::launch_fwd_combine(tm, a, c->num_sms, (cudaStream_t)stream))

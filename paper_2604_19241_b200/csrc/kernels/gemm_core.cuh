@@ -36,7 +36,7 @@ constexpr int TASK_STOP = -1;
 
 // One GEMM tile task. Meaning of the fields per mode is documented at each
 // mode's producer/epilogue.
-struct TileDesc {
+struct alignas(16) TileDesc {
   int e;      // local expert
   int m0;     // first row of A / of the row-indexed outputs (wgrad: output row)
   int n0;     // output column start
@@ -46,9 +46,10 @@ struct TileDesc {
   int pad0, pad1;
 };
 
+constexpr int STAGES_MAX = 6;  // the CTA-pair engine runs 6 stages of 32 KB
 struct GemmSmem {
-  uint64_t full[STAGES];
-  uint64_t empty[STAGES];
+  uint64_t full[STAGES_MAX];
+  uint64_t empty[STAGES_MAX];
   uint64_t tfull[ACC_STAGES];
   uint64_t tempty[ACC_STAGES];
   uint64_t rfull[RING];
@@ -58,6 +59,9 @@ struct GemmSmem {
   int ring[RING];
   uint32_t tmem_base;
   int bcast;
+  int pend[2];      // CTA pair: first non-pre task id of each CTA (leader's copy)
+  int post_ids[4];  // CTA pair: claimed non-tile ids to hand out after the GEMM phase
+  int post_n;
   // comm role (runs before the CTA enters the GEMM roles; reuses the stage buffers)
   uint64_t cbar[48];      // one mbarrier per bulk-copy slot
   uint32_t cphase[4];     // per issuer: parity bit per owned slot (carried across comm tasks)

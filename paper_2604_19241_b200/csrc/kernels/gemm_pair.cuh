@@ -1,0 +1,228 @@
+// CTA-pair (cta_group::2) variant of the grouped-GEMM engine.
+//
+// A cluster of two CTAs on one TPC computes 256 x 256 tiles: CTA r stages rows
+// [128r, 128r+128) of A and columns [128r, 128r+128) of B (32 KB per stage and CTA, 6 stages),
+// the leader (rank 0) issues tcgen05.mma.cta_group::2 (M=256, N=256, K=16) which reads both
+// CTAs' shared memory and accumulates rows [128r, ..) into CTA r's TMEM. Versus the single-CTA
+// engine every B tile is fetched once per pair instead of twice and the pipeline is 6 deep.
+//
+// Roles (per CTA, 256 threads):  warp 0 TMA producer (both CTAs), warp 1 MMA issuer (leader),
+// warp 2 TMEM owner (both, cta_group::2 allocation), warp 3 scheduler (leader: claims task ids,
+// decodes tiles, resolves scoreboard waits, writes the tile into both CTAs' rings over DSMEM),
+// warps 4-7 epilogue (both, each on its own 128 rows).
+// Barrier ownership: full[s] (leader, 2 arrivals + tx of both CTAs), empty[s] (each CTA, one
+// multicast MMA commit), tfull[a] (each CTA, multicast commit), tempty[a] (leader, 8 epilogue
+// warps), rfull[q] (each CTA, leader's scheduler), rempty[q] (leader, 6 local + 5 remote).
+#pragma once
+#include "gemm_engine.cuh"
+
+namespace eplab_dev {
+
+constexpr int P_STAGES = 6;
+constexpr uint32_t P_HALF_BYTES = 128 * BK * 2;  // 16 KB: one CTA's A rows or B columns
+constexpr uint32_t P_STAGE_BYTES = 2 * P_HALF_BYTES;
+static_assert(P_STAGES * P_STAGE_BYTES == TILES_BYTES, "pair stages reuse the single-CTA smem map");
+
+__device__ __forceinline__ void gemm_setup_pair(GemmSmem* S, uint32_t rank) {
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < P_STAGES; ++i) {
+      mbar_init(&S->full[i], 2);  // leader's expect_tx arrival + the peer's arrival
+      mbar_init(&S->empty[i], 1);
+    }
+    for (int i = 0; i < ACC_STAGES; ++i) {
+      mbar_init(&S->tfull[i], 1);
+      mbar_init(&S->tempty[i], 8);  // 4 epilogue warps per CTA
+    }
+    for (int i = 0; i < RING; ++i) {
+      mbar_init(&S->rfull[i], 1);
+      mbar_init(&S->rempty[i], 11);  // leader: producer, mma, 4 epi; peer: producer, 4 epi
+    }
+    for (int i = 0; i < 48; ++i) mbar_init(&S->cbar[i], 1);
+    for (int i = 0; i < 4; ++i) S->cphase[i] = 0;
+    S->bcast = TASK_STOP;
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_pair(&S->tmem_base, TMEM_COLS);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+}
+
+__device__ __forceinline__ void gemm_teardown_pair(GemmSmem* S) {
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if ((threadIdx.x >> 5) == 2) tmem_dealloc_pair(S->tmem_base, TMEM_COLS);
+}
+
+// Both CTAs call this after exchanging their first non-pre task ids into the leader's
+// S->pend[0..1] (ascending). Afterwards the leader's S->post_ids[0..S->post_n) hold the claimed
+// ids that are not tiles (to be handed out by the caller).
+template <class Mode>
+__device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& tm,
+                                uint8_t* tiles_smem, GemmSmem* S, int tile_lo, int tile_hi,
+                                int* __restrict__ cursor, const Timeline& tl, uint32_t rank) {
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = lane_id();
+  uint8_t* sA = tiles_smem;
+  uint8_t* sB = tiles_smem + P_STAGES * P_HALF_BYTES;
+  const bool leader = rank == 0;
+
+  if (warp == 3) {
+    if (leader && lane == 0) {
+      // ---------------- scheduler (leader)
+      int np = 0;
+      S->post_n = 0;
+      if (S->pend[1] < S->pend[0]) {
+        const int t0 = S->pend[0];
+        S->pend[0] = S->pend[1];
+        S->pend[1] = t0;
+      }
+      for (int it = 0;; ++it) {
+        const int slot = it % RING;
+        int id;
+        if (np < 2) {
+          id = S->pend[np++];
+        } else {
+          id = atomicAdd(cursor, 1);
+        }
+        const bool is_tile = id >= tile_lo && id < tile_hi;
+        if (!is_tile) {  // pending ids are ascending: a later pending id is not a tile either
+          S->post_ids[S->post_n++] = id;
+          if (np < 2) S->post_ids[S->post_n++] = S->pend[np++];
+        }
+        TileDesc td{};
+        if (is_tile) {
+          td = Mode::tile_pair(args, id - tile_lo);
+          Mode::before_loads_pair(args, td);
+        }
+        mbar_wait_cluster(&S->rempty[slot], ((it / RING) & 1) ^ 1);
+        const int rv = is_tile ? id - tile_lo : TASK_STOP;
+        S->ring[slot] = rv;
+        S->ring_td[slot] = td;
+        // the peer's ring slot over DSMEM, then release both rfull barriers (cluster scope)
+        const uint32_t peer_ring = mapa_shared(smem_u32(&S->ring[slot]), 1);
+        const uint32_t peer_td = mapa_shared(smem_u32(&S->ring_td[slot]), 1);
+        st_cluster_u32(peer_ring, (uint32_t)rv);
+        const int4* tdv = reinterpret_cast<const int4*>(&td);
+        st_cluster_v4(peer_td, tdv[0]);
+        st_cluster_v4(peer_td + 16, tdv[1]);
+        fence_acq_rel_cluster();  // the descriptor stores before the peer's rfull arrival
+        mbar_arrive_cluster(mapa_shared(smem_u32(&S->rfull[slot]), 0));
+        mbar_arrive_cluster(mapa_shared(smem_u32(&S->rfull[slot]), 1));
+        if (!is_tile) break;
+      }
+    }
+  } else if (warp == 0) {
+    // ---------------- TMA producer (both CTAs)
+    if (lane == 0) {
+      for (int i = 0; i < 8; ++i) tma_prefetch_desc(&tm.m[i]);
+      const uint32_t rempty0 = mapa_shared(smem_u32(&S->rempty[0]), 0);
+      uint32_t stage = 0, phase = 0;
+      for (int it = 0;; ++it) {
+        const int slot = it % RING;
+        mbar_wait_cluster(&S->rfull[slot], (it / RING) & 1);
+        const int t = S->ring[slot];
+        const TileDesc td = S->ring_td[slot];
+        mbar_arrive_cluster(rempty0 + slot * 8);
+        if (t == TASK_STOP) break;
+        fence_proxy_async_global();
+        if (leader) S->tstart[it & 7] = globaltimer();
+        for (int kb = 0; kb < td.nkb; ++kb) {
+          mbar_wait(&S->empty[stage], phase ^ 1);
+          const uint32_t full0 = mapa_shared(smem_u32(&S->full[stage]), 0);
+          if (leader)
+            mbar_arrive_expect_tx(&S->full[stage], 2 * P_STAGE_BYTES);
+          else
+            mbar_arrive_cluster(full0);
+          Mode::load_a_pair(args, tm, full0, sA + stage * P_HALF_BYTES, td, kb, rank);
+          Mode::load_b_pair(args, tm, full0, sB + stage * P_HALF_BYTES, td, kb, rank);
+          if (++stage == P_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- UMMA issuer (leader)
+    if (leader && lane == 0) {
+      const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+      uint32_t stage = 0, phase = 0;
+      for (int it = 0;; ++it) {
+        const int slot = it % RING;
+        mbar_wait_cluster(&S->rfull[slot], (it / RING) & 1);
+        const int t = S->ring[slot];
+        const TileDesc td = S->ring_td[slot];
+        mbar_arrive(&S->rempty[slot]);
+        if (t == TASK_STOP) break;
+        const int amn = Mode::a_mn(td), bmn = Mode::b_mn(td);
+        const uint32_t idesc = make_idesc(2 * BM, BN, amn, bmn);
+        const uint32_t acc = it & 1;
+        mbar_wait_cluster(&S->tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = S->tmem_base + acc * BN;
+        for (int kb = 0; kb < td.nkb; ++kb) {
+          mbar_wait(&S->full[stage], phase);
+          tc_fence_after();
+          const uint32_t as = a0 + stage * P_HALF_BYTES;
+          const uint32_t bs = b0 + stage * P_HALF_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = amn ? make_sdesc(as + k * 2048, 8192, 1024)
+                                    : make_sdesc(as + k * 32, 16, 1024);
+            const uint64_t bd = bmn ? make_sdesc(bs + k * 2048, 8192, 1024)
+                                    : make_sdesc(bs + k * 32, 16, 1024);
+            umma_bf16_pair(d, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit_pair(&S->empty[stage]);
+          if (++stage == P_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair(&S->tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue (both CTAs): this CTA's 128 rows of the 256-row tile
+    const int q = warp & 3;
+    const int r = q * 32 + (int)lane;
+    const uint32_t rempty0 = mapa_shared(smem_u32(&S->rempty[0]), 0);
+    const uint32_t tempty0 = mapa_shared(smem_u32(&S->tempty[0]), 0);
+    for (int it = 0;; ++it) {
+      const int slot = it % RING;
+      mbar_wait_cluster(&S->rfull[slot], (it / RING) & 1);
+      const int t = S->ring[slot];
+      const TileDesc td = S->ring_td[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(rempty0 + slot * 8);
+      if (t == TASK_STOP) {
+        if (lane == 0) tma_store_wait<0>();
+        break;
+      }
+      const TileDesc half = Mode::half_of(td, rank);
+      const bool work = Mode::half_has_work(half);
+      if (work) Mode::epilogue_prefetch(args, half, r);
+      const uint32_t acc = it & 1;
+      mbar_wait(&S->tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = S->tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
+      if (work) Mode::epilogue(args, tm, half, taddr, r, tiles_smem + TILES_BYTES + q * EPI_WARP_BYTES);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
+      if (Mode::HAS_TILE_DONE || tl.rec) {
+        epi_bar();
+        if (warp == 4 && lane == 0) {
+          if (Mode::HAS_TILE_DONE && work) Mode::tile_done(args, half);
+          if (leader) timeline_push(tl, S->tstart[it & 7], globaltimer(), ROLE_COMP, t + tile_lo);
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace eplab_dev

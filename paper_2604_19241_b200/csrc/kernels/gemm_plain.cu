@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "gemm_engine.cuh"
+#include "gemm_pair.cuh"
 #include "tma_host.hpp"
 #include "eplab_b200.h"
 
@@ -108,6 +109,69 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   gemm_teardown(S);
 }
 
+
+// CTA-pair versions: tiles are 256 rows (two 128-row halves) x 256 columns.
+struct ModeNTPair : ModeNT {
+  __device__ static TileDesc tile_pair(const Args& a, int t) { return a.tiles[t]; }
+  __device__ static void before_loads_pair(const Args&, const TileDesc&) {}
+  __device__ static void load_a_pair(const Args&, const TmaSet& tm, uint32_t bar, uint8_t* s,
+                                     const TileDesc& td, int kb, uint32_t rank) {
+    tma_load_2d_pair(&tm.m[0], bar, s, kb * BK, td.m0 + 128 * rank);
+  }
+  __device__ static void load_b_pair(const Args& a, const TmaSet& tm, uint32_t bar, uint8_t* s,
+                                     const TileDesc& td, int kb, uint32_t rank) {
+    tma_load_2d_pair(&tm.m[2], bar, s, kb * BK, td.e * a.n_per_expert + td.n0 + 128 * rank);
+  }
+  __device__ static TileDesc half_of(const TileDesc& td, uint32_t rank) {
+    TileDesc h = td;
+    h.m0 = td.m0 + 128 * rank;
+    h.rows = max(0, min(128, td.rows - 128 * (int)rank));
+    return h;
+  }
+  __device__ static bool half_has_work(const TileDesc& h) { return h.rows > 0; }
+};
+
+struct ModeTNPair : ModeTN {
+  __device__ static TileDesc tile_pair(const Args& a, int t) { return a.tiles[t]; }
+  __device__ static void before_loads_pair(const Args&, const TileDesc&) {}
+  __device__ static void load_a_pair(const Args&, const TmaSet& tm, uint32_t bar, uint8_t* s,
+                                     const TileDesc& td, int kb, uint32_t rank) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+      tma_load_2d_pair(&tm.m[0], bar, s + i * 8192, td.m0 + 128 * rank + 64 * i, td.kb0 + kb * BK);
+  }
+  __device__ static void load_b_pair(const Args&, const TmaSet& tm, uint32_t bar, uint8_t* s,
+                                     const TileDesc& td, int kb, uint32_t rank) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+      tma_load_2d_pair(&tm.m[1], bar, s + i * 8192, td.n0 + 128 * rank + 64 * i, td.kb0 + kb * BK);
+  }
+  __device__ static TileDesc half_of(const TileDesc& td, uint32_t rank) {
+    TileDesc h = td;
+    h.m0 = td.m0 + 128 * rank;
+    return h;
+  }
+  __device__ static bool half_has_work(const TileDesc&) { return true; }
+};
+
+template <class Mode>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    plain_gemm_pair_kernel(const __grid_constant__ TmaSet tm, const typename Mode::Args args,
+                           int ntiles, int* cursor) {
+  extern __shared__ uint8_t raw_smem[];
+  uint8_t* base = smem_aligned(raw_smem);
+  GemmSmem* S = reinterpret_cast<GemmSmem*>(base + TILES_BYTES + EPI_BYTES);
+  const uint32_t rank = cluster_ctarank();
+  gemm_setup_pair(S, rank);
+  if (threadIdx.x == 0) {
+    const int id = atomicAdd(cursor, 1);
+    st_cluster_u32(mapa_shared(smem_u32(&S->pend[rank]), 0), (uint32_t)id);
+  }
+  cluster_sync_all();
+  gemm_roles_pair<Mode>(args, tm, base, S, 0, ntiles, cursor, Timeline{nullptr, nullptr, 0}, rank);
+  gemm_teardown_pair(S);
+}
+
 }  // namespace eplab_dev
 
 using namespace eplab_dev;
@@ -137,6 +201,32 @@ int launch_plain(const TmaSet& tm, const typename Mode::Args& args, const TileDe
   int grid = num_sms();
   if (grid > ntiles) grid = ntiles > 0 ? ntiles : 1;
   plain_gemm_kernel<Mode><<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, st>>>(tm, args, ntiles, d_cursor);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+template <class Mode>
+int launch_plain_pair(const TmaSet& tm, const typename Mode::Args& args, int ntiles, int* d_cursor,
+                      cudaStream_t st) {
+  static bool attr = false;
+  auto fn = plain_gemm_pair_kernel<Mode>;
+  if (!attr) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM_BYTES);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  cudaMemsetAsync(d_cursor, 0, sizeof(int), st);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((num_sms() / 2) * 2);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = GEMM_SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, fn, tm, args, ntiles, d_cursor);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 }  // namespace
@@ -207,6 +297,72 @@ int eplab_grouped_gemm_tn(const void* A, const void* B, void* C, int M_total, in
     tm.m[1] = tm.m[2] = tm.m[3] = tm.m[4] = tm.m[5] = tm.m[6] = tm.m[7] = eplab_host::make_bf16_map(B, M_total, NB, NB, 64, 64);
     ModeTN::Args args{d_tiles, (__nv_bfloat16*)C, NB, (long long)NA * NB};
     return launch_plain<ModeTN>(tm, args, d_tiles, (int)tiles.size(), d_cursor, st);
+  } catch (...) {
+    return 1;
+  }
+}
+
+// CTA-pair (cta_group::2) versions of the two grouped GEMMs (same arguments).
+int eplab_grouped_gemm_nt_pair(const void* A, const void* B, void* C, int M_total, int N, int K,
+                               int n_experts, const int* seg_start, const int* seg_rows,
+                               void* d_workspace, void* stream) {
+  try {
+    std::vector<TileDesc> tiles;
+    for (int e = 0; e < n_experts; ++e)
+      for (int m = 0; m < seg_rows[e]; m += 2 * BM)
+        for (int n = 0; n < N; n += BN) {
+          TileDesc t{};
+          t.e = e;
+          t.m0 = seg_start[e] + m;
+          t.n0 = n;
+          t.rows = seg_rows[e] - m < 2 * BM ? seg_rows[e] - m : 2 * BM;
+          t.nkb = K / BK;
+          tiles.push_back(t);
+        }
+    cudaStream_t st = (cudaStream_t)stream;
+    TileDesc* d_tiles = (TileDesc*)d_workspace;
+    int* d_cursor = (int*)((char*)d_workspace + sizeof(TileDesc) * tiles.size());
+    cudaMemcpyAsync(d_tiles, tiles.data(), sizeof(TileDesc) * tiles.size(),
+                    cudaMemcpyHostToDevice, st);
+    TmaSet tm;
+    tm.m[0] = eplab_host::make_bf16_map(A, M_total, K, K, 64, BM);
+    tm.m[1] = tm.m[3] = tm.m[4] = tm.m[5] = tm.m[6] = tm.m[7] = tm.m[0];
+    tm.m[2] = eplab_host::make_bf16_map(B, (uint64_t)n_experts * N, K, K, 64, 128);
+    ModeNT::Args args{d_tiles, (__nv_bfloat16*)C, N, N};
+    return launch_plain_pair<ModeNTPair>(tm, args, (int)tiles.size(), d_cursor, st);
+  } catch (...) {
+    return 1;
+  }
+}
+
+int eplab_grouped_gemm_tn_pair(const void* A, const void* B, void* C, int M_total, int NA, int NB,
+                               int n_experts, const int* seg_start, const int* seg_rows_padded,
+                               void* d_workspace, void* stream) {
+  try {
+    std::vector<TileDesc> tiles;
+    for (int e = 0; e < n_experts; ++e)
+      for (int m = 0; m < NA; m += 2 * BM)
+        for (int n = 0; n < NB; n += BN) {
+          TileDesc t{};
+          t.e = e;
+          t.m0 = m;
+          t.n0 = n;
+          t.rows = 2 * BM;
+          t.kb0 = seg_start[e];
+          t.nkb = seg_rows_padded[e] / BK;
+          tiles.push_back(t);
+        }
+    cudaStream_t st = (cudaStream_t)stream;
+    TileDesc* d_tiles = (TileDesc*)d_workspace;
+    int* d_cursor = (int*)((char*)d_workspace + sizeof(TileDesc) * tiles.size());
+    cudaMemcpyAsync(d_tiles, tiles.data(), sizeof(TileDesc) * tiles.size(),
+                    cudaMemcpyHostToDevice, st);
+    TmaSet tm;
+    tm.m[0] = eplab_host::make_bf16_map(A, M_total, NA, NA, 64, 64);
+    tm.m[1] = eplab_host::make_bf16_map(B, M_total, NB, NB, 64, 64);
+    tm.m[2] = tm.m[3] = tm.m[4] = tm.m[5] = tm.m[6] = tm.m[7] = tm.m[0];
+    ModeTN::Args args{d_tiles, (__nv_bfloat16*)C, NB, (long long)NA * NB};
+    return launch_plain_pair<ModeTNPair>(tm, args, (int)tiles.size(), d_cursor, st);
   } catch (...) {
     return 1;
   }

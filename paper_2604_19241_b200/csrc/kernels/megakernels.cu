@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include "gemm_engine.cuh"
+#include "gemm_pair.cuh"
 #include "moe_common.cuh"
 
 namespace eplab_dev {
@@ -151,6 +152,77 @@ __device__ __forceinline__ TileDesc tn_tile(const Dims& d, const PlanDev& p, int
   td.pad0 = td.n0 / BN;
   td.pad1 = 1;  // transposed tile
   return td;
+}
+
+// CTA-pair tiles: 256 token rows (two 128-row blocks of one expert; the second may be empty
+// when the expert has an odd number of blocks) x column block, grouped raster of 8 pairs.
+constexpr int RASTER_GP = 8;
+__device__ __forceinline__ int expert_of_pair(const PlanDev& p, int epr, long long g) {
+  int lo = 0, hi = epr - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if ((long long)p.mpair_pre[mid] <= g)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+__device__ __forceinline__ TileDesc nt_tile_pair(const Dims& d, const PlanDev& p, int t, int nb,
+                                                 int bn_cols, int nkb) {
+  const int e = expert_of_pair(p, d.epr, (long long)t / nb);
+  const int local = t - p.mpair_pre[e] * nb;
+  const int mps = p.mpair_pre[e + 1] - p.mpair_pre[e];
+  const int g = local / (RASTER_GP * nb);
+  const int gsz = min(RASTER_GP, mps - g * RASTER_GP);
+  const int r = local - g * RASTER_GP * nb;
+  const int nbk = r / gsz, mp = g * RASTER_GP + r % gsz;
+  TileDesc td;
+  const int ge = d.rank * d.epr + e;
+  td.e = e;
+  td.m0 = p.sb_all[ge] + mp * 2 * BM;
+  td.rows = min(2 * BM, p.rt_all[ge] - mp * 2 * BM);
+  td.n0 = nbk * bn_cols;
+  td.kb0 = 0;
+  td.nkb = nkb;
+  td.pad0 = nbk;
+  td.pad1 = 0;
+  return td;
+}
+constexpr int TN_GP = 4;
+__device__ __forceinline__ TileDesc tn_tile_pair(const Dims& d, const PlanDev& p, int t, int NO,
+                                                 int KO) {
+  const int mb = NO / (2 * BM), nb = KO / BN, per_e = mb * nb;
+  TileDesc td;
+  td.e = t / per_e;
+  const int l = t - td.e * per_e;
+  const int g = l / (TN_GP * nb);
+  const int gsz = min(TN_GP, mb - g * TN_GP);
+  const int r = l - g * TN_GP * nb;
+  td.m0 = (g * TN_GP + r % gsz) * 2 * BM;
+  td.n0 = (r / gsz) * BN;
+  const int ge = d.rank * d.epr + td.e;
+  td.kb0 = p.sb_all[ge];
+  td.nkb = p.mblocks[td.e] * (BM / BK);
+  td.rows = 2 * BM;
+  td.pad0 = td.n0 / BN;
+  td.pad1 = 1;
+  return td;
+}
+__device__ __forceinline__ TileDesc half_tile(const TileDesc& td, uint32_t rank) {
+  TileDesc h = td;
+  h.m0 = td.m0 + BM * (int)rank;
+  h.rows = td.pad1 ? BM : max(0, min(BM, td.rows - BM * (int)rank));
+  return h;
+}
+// scoreboard wait of an NT pair tile: both 128-row blocks (the second only if it has rows)
+__device__ __forceinline__ void wait_pair_rows(const MkArgs& a, int ph, const TileDesc& td, int site) {
+  const SymPtrs& me = a.peers.p[a.d.rank];
+  const int g = td.m0 >> 7;
+  wait_geq_sys(rg_counter(me, a.d, ph, a.par, g), (uint32_t)min(BM, td.rows), a.timeout_ns, a.err, site, g);
+  if (td.rows > BM)
+    wait_geq_sys(rg_counter(me, a.d, ph, a.par, g + 1), (uint32_t)(td.rows - BM), a.timeout_ns, a.err, site,
+                 g + 1);
 }
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
@@ -464,6 +536,21 @@ struct ModeUp {
                  30, td.m0 >> 7);
   }
   __device__ static void epilogue_prefetch(const Args&, const TileDesc&, int) {}
+  // ---- CTA pair: rank 0 stages the gate rows, rank 1 the up rows of the same f-block
+  __device__ static TileDesc tile_pair(const Args& a, int t) {
+    return nt_tile_pair(a.d, a.p, t, a.d.F / 128, 128, a.d.H / BK);
+  }
+  __device__ static void before_loads_pair(const Args& a, const TileDesc& td) { wait_pair_rows(a, 0, td, 30); }
+  __device__ static void load_a_pair(const Args&, const TmaSet& tm, uint32_t bar, uint8_t* s,
+                                     const TileDesc& td, int kb, uint32_t rank) {
+    tma_load_2d_pair(&tm.m[0], bar, s, kb * BK, td.m0 + BM * rank);
+  }
+  __device__ static void load_b_pair(const Args& a, const TmaSet& tm, uint32_t bar, uint8_t* s,
+                                     const TileDesc& td, int kb, uint32_t rank) {
+    tma_load_2d_pair(&tm.m[1], bar, s, kb * BK, td.e * 2 * a.d.F + td.n0 + rank * a.d.F);
+  }
+  __device__ static TileDesc half_of(const TileDesc& td, uint32_t rank) { return half_tile(td, rank); }
+  __device__ static bool half_has_work(const TileDesc& h) { return h.rows > 0; }
   __device__ static void load_a(const Args&, const TmaSet& tm, uint64_t* bar, uint8_t* s,
                                 const TileDesc& td, int kb) {
     tma_load_2d(&tm.m[0], bar, s, kb * BK, td.m0);
@@ -538,6 +625,20 @@ struct ModeDown {
   using Args = MkArgs;
   static constexpr bool HAS_TILE_DONE = false;
   __device__ static void epilogue_prefetch(const Args&, const TileDesc&, int) {}
+  __device__ static TileDesc tile_pair(const Args& a, int t) {
+    return nt_tile_pair(a.d, a.p, t, a.d.H / BN, BN, a.d.F / BK);
+  }
+  __device__ static void before_loads_pair(const Args&, const TileDesc&) {}
+  __device__ static void load_a_pair(const Args&, const TmaSet& tm, uint32_t bar, uint8_t* s,
+                                     const TileDesc& td, int kb, uint32_t rank) {
+    tma_load_2d_pair(&tm.m[0], bar, s, kb * BK, td.m0 + BM * rank);
+  }
+  __device__ static void load_b_pair(const Args& a, const TmaSet& tm, uint32_t bar, uint8_t* s,
+                                     const TileDesc& td, int kb, uint32_t rank) {
+    tma_load_2d_pair(&tm.m[2], bar, s, kb * BK, td.e * a.d.H + td.n0 + BM * rank);
+  }
+  __device__ static TileDesc half_of(const TileDesc& td, uint32_t rank) { return half_tile(td, rank); }
+  __device__ static bool half_has_work(const TileDesc& h) { return h.rows > 0; }
   __device__ static int a_mn(const TileDesc&) { return 0; }
   __device__ static int b_mn(const TileDesc&) { return 0; }
   __device__ static TileDesc tile(const Args& a, int t) {
@@ -596,6 +697,38 @@ __device__ __forceinline__ void wgrad_store(const CUtensorMap* map, const TileDe
 struct ModeDgradDown {
   using Args = MkArgs;
   static constexpr bool HAS_TILE_DONE = true;
+  __device__ static int n_dgrad_pair(const Args& a) { return a.p.mpair_pre[a.d.epr] * (a.d.F / BN); }
+  __device__ static TileDesc tile_pair(const Args& a, int t) {
+    const int nd = n_dgrad_pair(a);
+    if (t < nd) return nt_tile_pair(a.d, a.p, t, a.d.F / BN, BN, a.d.H / BK);
+    return tn_tile_pair(a.d, a.p, t - nd, a.d.H, a.d.F);
+  }
+  __device__ static void before_loads_pair(const Args& a, const TileDesc& td) {
+    if (!td.pad1)
+      wait_pair_rows(a, 1, td, 31);
+    else
+      wait_geq_sys(a.wg_cnt + td.e * (a.d.F / BN) + td.pad0, (uint32_t)a.p.mblocks[td.e],
+                   a.timeout_ns, a.err, 32, td.e * 1000 + td.pad0);
+  }
+  __device__ static void load_a_pair(const Args&, const TmaSet& tm, uint32_t bar, uint8_t* s,
+                                     const TileDesc& td, int kb, uint32_t rank) {
+    if (!td.pad1) {
+      tma_load_2d_pair(&tm.m[0], bar, s, kb * BK, td.m0 + BM * rank);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        tma_load_2d_pair(&tm.m[2], bar, s + i * 8192, td.m0 + BM * rank + 64 * i, td.kb0 + kb * BK);
+    }
+  }
+  __device__ static void load_b_pair(const Args& a, const TmaSet& tm, uint32_t bar, uint8_t* s,
+                                     const TileDesc& td, int kb, uint32_t rank) {
+    const CUtensorMap* map = td.pad1 ? &tm.m[3] : &tm.m[1];
+    const int row = td.pad1 ? td.kb0 + kb * BK : td.e * a.d.H + kb * BK;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) tma_load_2d_pair(map, bar, s + i * 8192, td.n0 + BM * rank + 64 * i, row);
+  }
+  __device__ static TileDesc half_of(const TileDesc& td, uint32_t rank) { return half_tile(td, rank); }
+  __device__ static bool half_has_work(const TileDesc& h) { return h.pad1 || h.rows > 0; }
   __device__ static int n_dgrad(const Args& a) { return a.p.mblock_pre[a.d.epr] * (a.d.F / BN); }
   __device__ static int a_mn(const TileDesc& td) { return td.pad1; }
   __device__ static int b_mn(const TileDesc&) { return 1; }
@@ -652,7 +785,7 @@ struct ModeDgradDown {
     const int F = a.d.F;
     if (td.pad1) {  // weight-gradient tile
       wgrad_store(&tm.m[6], td, a.d.H, taddr, r, stg);
-      return;
+      return;  // (pair: td is this CTA's 128-row half of the 256-row dW tile)
     }
     const uint32_t lane = r & 31;
     const size_t m = (size_t)td.m0 + r;
@@ -755,6 +888,32 @@ struct ModeDgradUp {
   using Args = MkArgs;
   static constexpr bool HAS_TILE_DONE = false;
   __device__ static void epilogue_prefetch(const Args&, const TileDesc&, int) {}
+  __device__ static int n_dgrad_pair(const Args& a) { return a.p.mpair_pre[a.d.epr] * (a.d.H / BN); }
+  __device__ static TileDesc tile_pair(const Args& a, int t) {
+    const int nd = n_dgrad_pair(a);
+    if (t < nd) return nt_tile_pair(a.d, a.p, t, a.d.H / BN, BN, 2 * a.d.F / BK);
+    return tn_tile_pair(a.d, a.p, t - nd, 2 * a.d.F, a.d.H);
+  }
+  __device__ static void before_loads_pair(const Args&, const TileDesc&) {}
+  __device__ static void load_a_pair(const Args&, const TmaSet& tm, uint32_t bar, uint8_t* s,
+                                     const TileDesc& td, int kb, uint32_t rank) {
+    if (!td.pad1) {
+      tma_load_2d_pair(&tm.m[0], bar, s, kb * BK, td.m0 + BM * rank);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        tma_load_2d_pair(&tm.m[2], bar, s + i * 8192, td.m0 + BM * rank + 64 * i, td.kb0 + kb * BK);
+    }
+  }
+  __device__ static void load_b_pair(const Args& a, const TmaSet& tm, uint32_t bar, uint8_t* s,
+                                     const TileDesc& td, int kb, uint32_t rank) {
+    const CUtensorMap* map = td.pad1 ? &tm.m[3] : &tm.m[1];
+    const int row = td.pad1 ? td.kb0 + kb * BK : td.e * 2 * a.d.F + kb * BK;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) tma_load_2d_pair(map, bar, s + i * 8192, td.n0 + BM * rank + 64 * i, row);
+  }
+  __device__ static TileDesc half_of(const TileDesc& td, uint32_t rank) { return half_tile(td, rank); }
+  __device__ static bool half_has_work(const TileDesc& h) { return h.pad1 || h.rows > 0; }
   __device__ static int n_dgrad(const Args& a) { return a.p.mblock_pre[a.d.epr] * (a.d.H / BN); }
   __device__ static int a_mn(const TileDesc& td) { return td.pad1; }
   __device__ static int b_mn(const TileDesc&) { return 1; }
@@ -873,6 +1032,77 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   gemm_teardown(S);
 }
 
+
+// CTA-pair MegaKernel: the same task space with 256-row (pair) tiles. Each CTA resolves
+// pre-tasks (comm / relay) on its own; the pair then enters the GEMM phase together (the
+// leader schedules tiles for both) and afterwards each CTA resolves post-tasks (reduce).
+template <int KIND, class Mode>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    megakernel_pair(const __grid_constant__ TmaSet tm, const __grid_constant__ MkArgs a) {
+  extern __shared__ uint8_t raw_smem[];
+  uint8_t* base = smem_aligned(raw_smem);
+  GemmSmem* S = reinterpret_cast<GemmSmem*>(base + TILES_BYTES + EPI_BYTES);
+  const uint32_t rank = cluster_ctarank();
+  const int ph = (KIND >= 2) ? 1 : 0;
+  const bool has_pre = (KIND == 0 || KIND == 2);
+  const bool has_post = (KIND == 1 || KIND == 3);
+  if (blockIdx.x == 0) {
+    const SymPtrs& me = a.peers.p[a.d.rank];
+    if (has_pre)
+      for (int g = threadIdx.x; g < a.d.RG_cap; g += blockDim.x) *rg_counter(me, a.d, ph, a.par ^ 1, g) = 0;
+    if (has_post)
+      for (int t = threadIdx.x; t < a.d.T_max; t += blockDim.x) *tok_counter(me, a.d, ph, a.par ^ 1, t) = 0;
+  }
+  gemm_setup_pair(S, rank);
+  const int n_pre = has_pre ? a.n_disp + a.n_relay : 0;
+  const int pairs = a.p.mpair_pre[a.d.epr];
+  int n_tiles = 0;
+  if (KIND == 0) n_tiles = pairs * (a.d.F / 128);
+  if (KIND == 1) n_tiles = pairs * (a.d.H / BN);
+  if (KIND == 2) n_tiles = pairs * (a.d.F / BN) + a.d.epr * (a.d.H / (2 * BM)) * (a.d.F / BN);
+  if (KIND == 3) n_tiles = pairs * (a.d.H / BN) + a.d.epr * (2 * a.d.F / (2 * BM)) * (a.d.H / BN);
+  const int n_post = has_post ? a.n_red : 0;
+  const int total = n_pre + n_tiles + n_post;
+
+  auto claim = [&]() {
+    __syncthreads();
+    if (threadIdx.x == 0) S->bcast = atomicAdd(a.cursor, 1);
+    __syncthreads();
+    return S->bcast;
+  };
+  int id = claim();
+  while (id < n_pre) {
+    const unsigned long long t0 = globaltimer();
+    if (id < a.n_disp)
+      comm_task(a, id, ph, S, base);
+    else
+      relay_task(a, id - a.n_disp, ph);
+    __syncthreads();
+    if (threadIdx.x == 0) timeline_push(a.tl, t0, globaltimer(), id < a.n_disp ? ROLE_COMM : ROLE_RELAY, id);
+    id = claim();
+  }
+  // pair up: the leader learns both CTAs' first non-pre ids
+  if (threadIdx.x == 0) st_cluster_u32(mapa_shared(smem_u32(&S->pend[rank]), 0), (uint32_t)id);
+  cluster_sync_all();
+  gemm_roles_pair<Mode>(a, tm, base, S, n_pre, n_pre + n_tiles, a.cursor, a.tl, rank);
+  cluster_sync_all();
+  if (threadIdx.x == 0) {
+    const int pn = (int)ld_cluster_u32(mapa_shared(smem_u32(&S->post_n), 0));
+    S->bcast = (int)rank < pn ? (int)ld_cluster_u32(mapa_shared(smem_u32(&S->post_ids[rank]), 0))
+                              : atomicAdd(a.cursor, 1);
+  }
+  __syncthreads();
+  id = S->bcast;
+  while (id < total) {
+    const unsigned long long t0 = globaltimer();
+    reduce_task(a, id - n_pre - n_tiles, ph);
+    __syncthreads();
+    if (threadIdx.x == 0) timeline_push(a.tl, t0, globaltimer(), ROLE_REDUCE, id);
+    id = claim();
+  }
+  gemm_teardown_pair(S);
+}
+
 }  // namespace eplab_dev
 
 // ------------------------------------------------------------------ host launchers
@@ -881,16 +1111,39 @@ using namespace eplab_dev;
 
 template <int KIND, class Mode>
 static int launch_mk(const TmaSet& tm, const MkArgs& a, int grid, cudaStream_t st) {
-  static bool attr = false;
-  auto fn = megakernel<KIND, Mode>;
-  if (!attr) {
+  static bool attr = false, attr_p = false;
+  cudaMemsetAsync(a.cursor, 0, sizeof(int), st);
+  if (!a.pair) {
+    auto fn = megakernel<KIND, Mode>;
+    if (!attr) {
+      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)GEMM_SMEM_BYTES) != cudaSuccess)
+        return 1;
+      attr = true;
+    }
+    fn<<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, st>>>(tm, a);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+  }
+  auto fn = megakernel_pair<KIND, Mode>;
+  if (!attr_p) {
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)GEMM_SMEM_BYTES) != cudaSuccess)
       return 1;
-    attr = true;
+    attr_p = true;
   }
-  cudaMemsetAsync(a.cursor, 0, sizeof(int), st);
-  fn<<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, st>>>(tm, a);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((grid / 2) * 2);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = GEMM_SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, fn, tm, a);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 

@@ -82,6 +82,7 @@ struct PlanDev {
   int* mblocks;             // [epr] 128-row blocks (= rowgroups) per local expert
   int* mblock_pre;          // [epr+1] prefix of mblocks (tile t of a GEMM with nb column
                             //   blocks belongs to expert e iff mblock_pre[e]*nb <= t < ..[e+1]*nb)
+  int* mpair_pre;           // [epr+1] prefix of ceil(mblocks/2) (256-row CTA-pair tiles)
   int* scalars;             // [0]=M_used rows (aligned), [1]=n_rowgroups, [2]=recv total
 };
 
@@ -133,6 +134,7 @@ struct MkArgs {
   unsigned long long timeout_ns;
   Timeline tl;
   int dbg;  // debug bits (experiments only): 1 = skip epilogue stores of the up GEMM
+  int pair;  // 1: CTA-pair (cta_group::2) engine
 };
 
 }  // namespace eplab_dev

@@ -102,14 +102,17 @@ __global__ void plan_global_kernel(Dims d, Peers peers, PlanDev p, int nchunks, 
         acc += cnt_s[e];
       }
     // local receive geometry: 128-row blocks per local expert and their prefix
-    int mp = 0;
+    int mp = 0, pp = 0;
     for (int el = 0; el < epr; ++el) {
       const int mb = (rt[me * epr + el] + 127) >> 7;
       p.mblocks[el] = mb;
       p.mblock_pre[el] = mp;
+      p.mpair_pre[el] = pp;
       mp += mb;
+      pp += (mb + 1) >> 1;
     }
     p.mblock_pre[epr] = mp;
+    p.mpair_pre[epr] = pp;
   }
   __syncthreads();
   // global offsets of my copies: O_all[dst][e_loc][me] = sum_{s<me} C_all[s][e]  (Eq. 1)

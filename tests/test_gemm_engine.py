@@ -24,9 +24,10 @@ def _iarr(v):
     return (ctypes.c_int * len(v))(*v)
 
 
+@pytest.mark.parametrize("pair", [False, True])
 @pytest.mark.parametrize("counts,N,K", [([128], 256, 64), ([300, 0, 77, 1024], 512, 256),
                                         ([1000, 513], 1536, 2048)])
-def test_grouped_nt(counts, N, K):
+def test_grouped_nt(counts, N, K, pair):
     lib = _lib()
     torch.manual_seed(0)
     starts, M = _seg(counts)
@@ -35,7 +36,8 @@ def test_grouped_nt(counts, N, K):
     B = (torch.randn(E, N, K, device="cuda") / K ** 0.5).bfloat16()
     C = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
     ws = torch.empty(64 << 20, device="cuda", dtype=torch.uint8)
-    rc = lib.eplab_grouped_gemm_nt(ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
+    fn = lib.eplab_grouped_gemm_nt_pair if pair else lib.eplab_grouped_gemm_nt
+    rc = fn(ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
                                    ctypes.c_void_p(C.data_ptr()), M, N, K, E, _iarr(starts),
                                    _iarr(counts), ctypes.c_void_p(ws.data_ptr()), None)
     assert rc == 0
@@ -50,9 +52,10 @@ def test_grouped_nt(counts, N, K):
         assert err <= 2e-2 * ref.abs().max().item() + 1e-2, (e, err)
 
 
-@pytest.mark.parametrize("counts,NA,NB", [([128], 128, 256), ([300, 0, 77], 256, 512),
+@pytest.mark.parametrize("pair", [False, True])
+@pytest.mark.parametrize("counts,NA,NB", [([128], 256, 256), ([300, 0, 77], 256, 512),
                                           ([1000, 513], 768, 1024)])
-def test_grouped_tn(counts, NA, NB):
+def test_grouped_tn(counts, NA, NB, pair):
     lib = _lib()
     torch.manual_seed(1)
     starts, M = _seg(counts)
@@ -66,7 +69,8 @@ def test_grouped_tn(counts, NA, NB):
     C = torch.full((E, NA, NB), 7.0, device="cuda", dtype=torch.bfloat16)
     ws = torch.empty(64 << 20, device="cuda", dtype=torch.uint8)
     padded = [(c + 127) // 128 * 128 for c in counts]
-    rc = lib.eplab_grouped_gemm_tn(ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(Bm.data_ptr()),
+    fn = lib.eplab_grouped_gemm_tn_pair if pair else lib.eplab_grouped_gemm_tn
+    rc = fn(ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(Bm.data_ptr()),
                                    ctypes.c_void_p(C.data_ptr()), M, NA, NB, E, _iarr(starts),
                                    _iarr(padded), ctypes.c_void_p(ws.data_ptr()), None)
     assert rc == 0

@@ -161,13 +161,13 @@ LatencyBreakdown predict_latency(const MoEShape& shape, const HardwareSpec& spec
 // --------------------------------------------------------------- B200 model of the MegaKernels
 // Calibrated constants of this implementation on B200 (DESIGN.md §Performance model).
 struct B200Calib {
-  double mu = 0.7695;             // tensor-pipe efficiency of the tile main loop (fitted, r01)
-  double tile_overhead = 0.0;     // per-tile hand-off cost not hidden behind the loop, s
-  double comm_bw_per_sm = 11.0e9; // B/s one comm CTA sustains (TMA bulk row copies, fitted)
-  double relay_bw_per_sm = 11.0e9;  // B/s one relay CTA sustains on HBM copies
-  double reduce_bw = 2.775e12;    // B/s of the reduce role when all SMs join (fitted)
-  double launch = 82.7e-6;        // per MegaKernel fixed cost: launch, prologue, pipeline fill
-  double epi_bw_per_sm = 25.9e9;  // B/s of epilogue traffic per SM (TMA stores, saved-input reads)
+  double mu = 0.8081;             // tensor-pipe efficiency of the tile main loop (fitted, r01)
+  double tile_overhead = 0.708e-6;  // per-tile hand-off cost not hidden behind the loop, s
+  double comm_bw_per_sm = 11.4e9; // B/s one comm CTA sustains (TMA bulk row copies, fitted)
+  double relay_bw_per_sm = 11.4e9;  // B/s one relay CTA sustains on HBM copies
+  double reduce_bw = 4.87e12;     // B/s of the reduce role when all SMs join (fitted)
+  double launch = 144.8e-6;       // per MegaKernel fixed cost: launch, prologue, pipeline fill
+  double epi_bw_per_sm = 70.0e9;  // B/s of epilogue traffic per SM (TMA stores, saved-input reads)
 };
 struct LayerPrediction {
   double fwd_dispatch = 0, fwd_combine = 0, bwd_dispatch = 0, bwd_combine = 0, total = 0;

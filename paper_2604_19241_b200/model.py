@@ -49,7 +49,7 @@ class LayerPrediction(C.Structure):
 
 
 # B200 calibration of this build (DESIGN.md §Performance model; refit by tools/calibrate_model.py)
-B200_CALIB = Calib(0.7695, 0.0, 11.0e9, 11.0e9, 2.775e12, 82.7e-6, 25.9e9)  # profiles/r01_perf_model_validation.md
+B200_CALIB = Calib(0.8081, 0.708e-6, 11.4e9, 11.4e9, 4.87e12, 144.8e-6, 70.0e9)  # profiles/r01_perf_model_validation.md (pair engine)
 
 
 def hw(world, n_sm=148, p_peak=1408.1e12, bw_hbm=6468.9e9, bw_nvl=770e9, w_sat=1024.0, tau_sync=1e-6):

@@ -346,11 +346,13 @@ __device__ void comm_task(const MkArgs& a, int task, int ph, GemmSmem* S, uint8_
   const Dims& d = a.d;
   const int k = d.topk, H = d.H, me = d.rank;
   const long long n = (long long)a.p.n_tok * k;
-  long long lo, hi;
-  even_slice(n, a.n_disp, task, lo, hi);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool relay_on = a.n_relay > 0;
-  for (long long b0 = lo; b0 < hi; b0 += GEMM_THREADS) {
+  // Rounds of 256 schedule items are dealt round-robin to the comm tasks, so all comm CTAs move
+  // through the priority order front to back together and the first rowgroups (the first GEMM
+  // tiles' inputs) land after ~1/n_disp of the single-slice time.
+  for (long long b0 = (long long)task * GEMM_THREADS; b0 < n; b0 += (long long)a.n_disp * GEMM_THREADS) {
+    const long long hi = n;
     const int cnt = (hi - b0) < GEMM_THREADS ? (int)(hi - b0) : GEMM_THREADS;
     // ---- parallel metadata: one thread per item. Writes the destination slot's return
     // address (forward) and, relay on, publishes duplicate slots right away: their flag means

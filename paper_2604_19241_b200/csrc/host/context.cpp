@@ -58,8 +58,10 @@ struct eplab_ctx {
   uint32_t* wg_cnt = nullptr;
   int* cursor = nullptr;
   int* err = nullptr;
-  // host-call staging (eplab_moe_step_host)
+  // host-call staging (eplab_moe_step_host) and its copy stream / events
   char* stage = nullptr;
+  cudaStream_t copy_st = nullptr;
+  cudaEvent_t ev_fwd = nullptr, ev_dy = nullptr, ev_y = nullptr;
   // fixed tensor maps
   CUtensorMap tm_recv_x_k{}, tm_recv_x_mn{}, tm_hact_k{}, tm_recv_dy_k{}, tm_recv_dy_mn{},
       tm_hw_mn{}, tm_dgu_k{}, tm_dgu_mn{};
@@ -278,6 +280,12 @@ int eplab_destroy(eplab_ctx* c) {
   cudaFree(c->sym);
   cudaFree(c->loc);
   cudaFree(c->stage);
+  if (c->copy_st) {
+    cudaStreamDestroy(c->copy_st);
+    cudaEventDestroy(c->ev_fwd);
+    cudaEventDestroy(c->ev_dy);
+    cudaEventDestroy(c->ev_y);
+  }
   if (c->tl_rec) cudaFree(c->tl_rec);
   if (c->tl_count) cudaFree(c->tl_count);
   delete c;
@@ -495,10 +503,19 @@ int eplab_moe_step_host(eplab_ctx* c, const int32_t* h_ids, const float* h_gw, i
                         const void* h_x, const void* h_dy, const void* w_up, const void* w_down,
                         void* h_y, void* h_dx, float* h_dgate, void* dw_up, void* dw_down,
                         void* stream) {
+  // Copies overlap compute on a side stream: dY's H2D runs under the forward MegaKernels and
+  // y's D2H under the backward ones; only the routing/x upload and the dx/dgate download are
+  // exposed. Host buffers should be pinned for the copies to be asynchronous.
   int rc = guarded([&] {
     validate(n_tok >= 0 && n_tok <= c->d.T_max, "n_tok exceeds max_tokens");
     CK(cudaSetDevice(c->device));
     cudaStream_t st = (cudaStream_t)stream;
+    if (!c->copy_st) {
+      CK(cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c->ev_fwd, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_dy, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_y, cudaEventDisableTiming));
+    }
     const size_t Tk = (size_t)c->d.T_max * c->d.topk, TH = (size_t)c->d.T_max * c->d.H * 2;
     char* s = c->stage;
     int32_t* ids = reinterpret_cast<int32_t*>(s);
@@ -512,13 +529,21 @@ int eplab_moe_step_host(eplab_ctx* c, const int32_t* h_ids, const float* h_gw, i
     CK(cudaMemcpyAsync(ids, h_ids, nk * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(gw, h_gw, nk * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(x, h_x, nh, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(dy, h_dy, nh, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(c->ev_fwd, st));  // previous step's users of dy are ordered before this
+    CK(cudaStreamWaitEvent(c->copy_st, c->ev_fwd, 0));
+    CK(cudaMemcpyAsync(dy, h_dy, nh, cudaMemcpyHostToDevice, c->copy_st));
+    CK(cudaEventRecord(c->ev_dy, c->copy_st));
     int r = eplab_moe_fwd(c, ids, gw, n_tok, x, w_up, w_down, y, stream);
-    if (!r) r = eplab_moe_bwd(c, dy, w_up, w_down, dx, dw_up, dw_down, dg, stream);
     if (r) throw Fail{r, eplab_host::last_error()};
-    CK(cudaMemcpyAsync(h_y, y, nh, cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(c->ev_y, st));
+    CK(cudaStreamWaitEvent(c->copy_st, c->ev_y, 0));
+    CK(cudaMemcpyAsync(h_y, y, nh, cudaMemcpyDeviceToHost, c->copy_st));
+    CK(cudaStreamWaitEvent(st, c->ev_dy, 0));
+    r = eplab_moe_bwd(c, dy, w_up, w_down, dx, dw_up, dw_down, dg, stream);
+    if (r) throw Fail{r, eplab_host::last_error()};
     CK(cudaMemcpyAsync(h_dx, dx, nh, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(h_dgate, dg, nk * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(c->copy_st));
     CK(cudaStreamSynchronize(st));
   });
   return rc;

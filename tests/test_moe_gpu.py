@@ -237,3 +237,28 @@ def test_empty_batch_and_validation_errors():
     with pytest.raises(m.EplabError):
         m.EpMoE(300, 256, 8, 2, 64)  # hidden not a multiple of 256
     layer.close()
+
+
+def test_step_host_equals_device_path():
+    """eplab_moe_step_host (host buffers, overlapped copies) == the device-resident calls."""
+    prob = Problem(1, 8, 2, 256, 512, 200, seed=9)
+    ref, _, _ = run_layer(prob)
+    m = moe()
+    L = m.EpMoE(256, 512, 8, 2, 200)
+    ids = torch.from_numpy(prob.sel.reshape(200, 2).copy()).pin_memory()
+    gw = torch.from_numpy(prob.gw.reshape(200, 2).copy()).pin_memory()
+    x = from_u16(prob.x[0], "cpu").pin_memory()
+    dy = from_u16(prob.dy[0], "cpu").pin_memory()
+    wu, wd = from_u16(prob.w_up), from_u16(prob.w_down)
+    y = torch.empty(200, 256, dtype=torch.bfloat16).pin_memory()
+    dx = torch.empty(200, 256, dtype=torch.bfloat16).pin_memory()
+    dg = torch.empty(200, 2, dtype=torch.float32).pin_memory()
+    dwu, dwd = torch.empty_like(wu), torch.empty_like(wd)
+    for _ in range(2):  # second call exercises the copy-stream / event reuse
+        L.step_host(ids, gw, x, dy, wu, wd, y, dx, dg, dwu, dwd)
+    L.check()
+    r = ref[0][0]
+    assert (to_u16(y) == r["y"]).all() and (to_u16(dx) == r["dx"]).all()
+    assert (dg.numpy() == r["dgate"]).all()
+    assert (to_u16(dwu) == r["dw_up"]).all() and (to_u16(dwd) == r["dw_down"]).all()
+    L.close()

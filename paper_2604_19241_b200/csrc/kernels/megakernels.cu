@@ -225,7 +225,7 @@ __device__ __forceinline__ void wait_pair_rows(const MkArgs& a, int ph, const Ti
                  g + 1);
 }
 
-__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+__device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
 // Even split of n into parts (sim.cpp:151-161).
 __device__ __forceinline__ void even_slice(long long n, int parts, int i, long long& lo,
@@ -828,7 +828,7 @@ struct ModeDgradDown {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const float dh = w * v[2 * q + h];
-            const float sg = 1.0f / (1.0f + __expf(-gg[h]));
+            const float sg = __fdividef(1.0f, 1.0f + __expf(-gg[h]));
             const float si = gg[h] * sg;
             const float ds = sg * (1.0f + gg[h] * (1.0f - sg));
             const float hh = __bfloat162float(__float2bfloat16_rn(si * uu[h]));

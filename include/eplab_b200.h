@@ -70,6 +70,21 @@ EPLAB_API int eplab_grouped_gemm_tn_pair(const void* d_A, const void* d_B, void*
                                          const int* seg_rows_padded, void* d_workspace,
                                          void* stream);
 
+/* ------------------------------------------------------- router
+ * The gating step in front of dispatch. The reference takes routing as input
+ * (routing.cpp sample_routing: k distinct experts per token + weights summing to 1); these
+ * produce the same topk_ids [T][k] int32 / gate_w [T][k] fp32 on device from router logits
+ * [T][E] fp32, ready for eplab_plan. Top-k descending, ties -> lower expert index.
+ * renorm = 1: softmax over the k selected logits (weights sum to 1, like sample_routing);
+ * renorm = 0: full softmax probabilities of the selected experts.
+ * Backward: dgate [T][k] (eplab_moe_bwd's d_dgate) -> dlogits [T][E].
+ * 1 <= topk <= min(32, E), E <= 1024. Bit-exact with oracle/eplab_oracle.c orc_router_topk. */
+EPLAB_API int eplab_router_topk(const float* d_logits, int n_tok, int n_experts, int topk, int renorm,
+                                int32_t* d_topk_ids, float* d_gate_w, void* stream);
+EPLAB_API int eplab_router_topk_bwd(const float* d_logits, const int32_t* d_topk_ids, const float* d_gate_w,
+                                    const float* d_dgate, int n_tok, int n_experts, int topk, int renorm,
+                                    float* d_dlogits, void* stream);
+
 
 /* ------------------------------------------------------- EP-MoE context (per rank) */
 

@@ -693,3 +693,100 @@ done:
   free(o);
   return 0;
 }
+
+/* ------------------------------------------------------------- router (§8 f1) */
+/* See eplab_oracle.h: semantics defined by this repo. */
+float orc_exp_portable(float x) {
+  if (!(x >= -87.0f)) return 0.0f;
+  const float n = rintf(x * 1.44269504088896341f);
+  float r = fmaf(-n, 0.693145751953125f, x);
+  r = fmaf(-n, 1.42860682030941723212e-6f, r);
+  float p = 1.98412698412698413e-4f;
+  p = fmaf(p, r, 1.38888888888888889e-3f);
+  p = fmaf(p, r, 8.33333333333333333e-3f);
+  p = fmaf(p, r, 4.16666666666666667e-2f);
+  p = fmaf(p, r, 1.66666666666666667e-1f);
+  p = fmaf(p, r, 0.5f);
+  p = fmaf(p, r, 1.0f);
+  p = fmaf(p, r, 1.0f);
+  const int e = (int)n;
+  uint32_t bits = (uint32_t)(e + 127) << 23;
+  float s;
+  memcpy(&s, &bits, 4);
+  return p * s;
+}
+
+static uint32_t rt_key(float v) {
+  uint32_t u;
+  memcpy(&u, &v, 4);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+/* sum_i exp(l_i - m) in the kernel's order: 32 lane partials (i = lane + 32q, q ascending),
+ * then v[l] += v[l ^ o] for o = 16, 8, 4, 2, 1 */
+static float rt_partition(const float* l, int E, float m) {
+  float v[32], nv[32];
+  for (int lane = 0; lane < 32; ++lane) {
+    float s = 0.0f;
+    for (int i = lane; i < E; i += 32) s = s + orc_exp_portable(l[i] - m);
+    v[lane] = s;
+  }
+  for (int o = 16; o; o >>= 1) {
+    for (int lane = 0; lane < 32; ++lane) nv[lane] = v[lane] + v[lane ^ o];
+    memcpy(v, nv, sizeof v);
+  }
+  return v[0];
+}
+
+static int rt_check(long long T, int E, int k) {
+  return (T < 0 || E < 1 || E > 1024 || k < 1 || k > 32 || k > E) ? 2 : 0;
+}
+
+int orc_router_topk(const float* logits, long long n_tok, int n_exp, int topk, int renorm, int32_t* ids,
+                    float* gw) {
+  if (rt_check(n_tok, n_exp, topk)) return 2;
+  for (long long t = 0; t < n_tok; ++t) {
+    const float* l = logits + t * n_exp;
+    unsigned char taken[1024];
+    memset(taken, 0, (size_t)n_exp);
+    float val[32], m = 0.0f, den = 0.0f;
+    for (int j = 0; j < topk; ++j) {
+      int best = -1;
+      for (int i = 0; i < n_exp; ++i)
+        if (!taken[i] && (best < 0 || rt_key(l[i]) > rt_key(l[best]))) best = i;
+      taken[best] = 1;
+      ids[t * topk + j] = best;
+      val[j] = l[best];
+      if (j == 0) m = val[0];
+      if (renorm) den = den + orc_exp_portable(val[j] - m);
+    }
+    if (!renorm) den = rt_partition(l, n_exp, m);
+    for (int j = 0; j < topk; ++j) gw[t * topk + j] = orc_exp_portable(val[j] - m) / den;
+  }
+  return 0;
+}
+
+int orc_router_topk_bwd(const float* logits, const int32_t* ids, const float* gw, const float* dgate,
+                        long long n_tok, int n_exp, int topk, int renorm, float* dlogits) {
+  if (rt_check(n_tok, n_exp, topk)) return 2;
+  for (long long t = 0; t < n_tok; ++t) {
+    const int32_t* id = ids + t * topk;
+    const float *w = gw + t * topk, *g = dgate + t * topk, *l = logits + t * n_exp;
+    float* out = dlogits + t * n_exp;
+    float S = 0.0f;
+    for (int j = 0; j < topk; ++j) S = fmaf(g[j], w[j], S);
+    if (renorm) {
+      for (int i = 0; i < n_exp; ++i) out[i] = 0.0f;
+      for (int j = 0; j < topk; ++j) out[id[j]] = w[j] * (g[j] - S);
+    } else {
+      int best = 0;
+      for (int i = 1; i < n_exp; ++i)
+        if (rt_key(l[i]) > rt_key(l[best])) best = i;
+      const float m = l[best], Z = rt_partition(l, n_exp, m);
+      for (int i = 0; i < n_exp; ++i) out[i] = (orc_exp_portable(l[i] - m) / Z) * -S;
+      for (int j = 0; j < topk; ++j)
+        out[id[j]] = (orc_exp_portable(l[id[j]] - m) / Z) * (g[j] - S);
+    }
+  }
+  return 0;
+}

@@ -129,6 +129,20 @@ int orc_moe_layer(const orc_layer_dims* d, const int32_t* sel, const float* gw,
                   const uint16_t* dy, uint16_t* y, uint16_t* dx, float* dgate, uint16_t* dw_up,
                   uint16_t* dw_down, int threads);
 
+/* ------------------------------------------------------------- router (§8 f1) */
+/* No reference implementation exists (the reference takes routing as input, routing.cpp:32-73;
+ * gating is described at PAPER.md:54-55). These define the product's router semantics, spelled
+ * operation by operation so the CUDA kernel (csrc/kernels/router.cu) is bit-exact with them:
+ * top-k by the IEEE total order of the logits (descending, ties -> lower index); renorm=1 softmax
+ * over the selected, renorm=0 full-softmax probabilities with Z summed in the warp's order
+ * (lane-strided partials, xor butterfly 16..1); exp from a fixed fmaf polynomial. Pinned by
+ * tests/test_oracle.py against an independent float64 softmax/top-k (numpy). */
+float orc_exp_portable(float x);
+int orc_router_topk(const float* logits, long long n_tok, int n_exp, int topk, int renorm, int32_t* ids,
+                    float* gw);
+int orc_router_topk_bwd(const float* logits, const int32_t* ids, const float* gw, const float* dgate,
+                        long long n_tok, int n_exp, int topk, int renorm, float* dlogits);
+
 /* Deterministic synthetic bf16 data: N(0,1)*scale via splitmix64 + Box-Muller. */
 void orc_fill_normal_bf16(uint16_t* out, long long n, uint64_t seed, float scale);
 

@@ -239,6 +239,30 @@ class Oracle(_Lib):
         self.lib.orc_fill_normal_bf16(_p(out), C.c_longlong(n), C.c_uint64(seed), C.c_float(scale))
         return out
 
+    # §8 f1 router (semantics defined in eplab_oracle.h)
+    def router_topk(self, logits, topk, renorm=True):
+        lg = np.ascontiguousarray(logits, np.float32)
+        T, E = lg.shape
+        ids = np.zeros((T, topk), np.int32)
+        gw = np.zeros((T, topk), np.float32)
+        rc = self.lib.orc_router_topk(_p(lg), C.c_longlong(T), E, topk, int(renorm), _p(ids), _p(gw))
+        if rc:
+            raise ValueError(f"router_topk rc={rc}")
+        return ids, gw
+
+    def router_topk_bwd(self, logits, ids, gw, dgate, renorm=True):
+        lg = np.ascontiguousarray(logits, np.float32)
+        T, E = lg.shape
+        ids = np.ascontiguousarray(ids, np.int32)
+        gw = np.ascontiguousarray(gw, np.float32)
+        dg = np.ascontiguousarray(dgate, np.float32)
+        out = np.zeros((T, E), np.float32)
+        rc = self.lib.orc_router_topk_bwd(_p(lg), _p(ids), _p(gw), _p(dg), C.c_longlong(T), E, ids.shape[1],
+                                          int(renorm), _p(out))
+        if rc:
+            raise ValueError(f"router_topk_bwd rc={rc}")
+        return out
+
 
 class Reference(_Lib):
     """The unmodified reference eplab (oracle/_ref)."""

@@ -663,21 +663,8 @@ int eplab_timeline_export(eplab_ctx* c, const char* path, double* overlap_frac) 
     CK(cudaMemset(c->tl_count, 0, 4));
     unsigned long long t0 = ~0ULL;
     for (auto& x : r) t0 = std::min(t0, x.t0);
-    static const char* names[4] = {"comm", "relay", "comp", "reduce"};
-    if (path && *path) {
-      std::ofstream f(path);
-      if (!f) throw Fail{EPLAB_ERR_VALIDATION, std::string("cannot write ") + path};
-      f << "{\"traceEvents\": [\n";
-      for (int i = 0; i < n; ++i) {
-        const uint32_t role = r[i].sm_role >> 16, sm = r[i].sm_role & 0xFFFF;
-        f << (i ? ",\n" : "") << "{\"name\": \"" << names[role & 3] << "\", \"cat\": \""
-          << names[role & 3] << "\", \"ph\": \"X\", \"ts\": " << (r[i].t0 - t0) * 1e-3
-          << ", \"dur\": " << (r[i].t1 - r[i].t0) * 1e-3 << ", \"pid\": " << c->d.rank
-          << ", \"tid\": " << sm << ", \"args\": {\"task\": " << r[i].task << "}}";
-      }
-      f << "\n], \"displayTimeUnit\": \"ns\"}\n";
-    }
-    if (overlap_frac) {
+    double overlap = 0.0;
+    {
       // sweep over interval endpoints
       std::vector<std::pair<unsigned long long, int>> ev;  // (time, +-1 comm | +-2 comp)
       for (auto& x : r) {
@@ -701,7 +688,47 @@ int eplab_timeline_export(eplab_ctx* c, const char* path, double* overlap_frac) 
         if (e.second == 2) ++comp;
         if (e.second == -2) --comp;
       }
-      *overlap_frac = t_comm > 0 ? t_both / t_comm : 0.0;
+      overlap = t_comm > 0 ? t_both / t_comm : 0.0;
+    }
+    if (overlap_frac) *overlap_frac = overlap;
+    static const char* names[4] = {"comm", "relay", "comp", "reduce"};
+    if (path && *path) {
+      std::ofstream f(path);
+      if (!f) throw Fail{EPLAB_ERR_VALIDATION, std::string("cannot write ") + path};
+      f << "{\"traceEvents\": [\n";
+      for (int i = 0; i < n; ++i) {
+        const uint32_t role = r[i].sm_role >> 16, sm = r[i].sm_role & 0xFFFF;
+        f << (i ? ",\n" : "") << "{\"name\": \"" << names[role & 3] << "\", \"cat\": \""
+          << names[role & 3] << "\", \"ph\": \"X\", \"ts\": " << (r[i].t0 - t0) * 1e-3
+          << ", \"dur\": " << (r[i].t1 - r[i].t0) * 1e-3 << ", \"pid\": " << c->d.rank
+          << ", \"tid\": " << sm << ", \"args\": {\"task\": " << r[i].task << "}}";
+      }
+      f << "\n], \"displayTimeUnit\": \"ns\"}\n";
+      // metrics next to the trace (trace.cpp:36-51 metrics_csv, :53-66 emit_trace path rule) from the
+      // measured timeline instead of the simulated one: phase ends, busy
+      // SM-seconds per role, GEMM start behind the scoreboard, overlap
+      double busy[4] = {0, 0, 0, 0}, end_role[4] = {0, 0, 0, 0}, first_comp = -1;
+      for (auto& x : r) {
+        const uint32_t role = (x.sm_role >> 16) & 3;
+        busy[role] += (x.t1 - x.t0) * 1e-9;
+        end_role[role] = std::max(end_role[role], (x.t1 - t0) * 1e-9);
+        if (role == ROLE_COMP && (first_comp < 0 || (x.t0 - t0) * 1e-9 < first_comp))
+          first_comp = (x.t0 - t0) * 1e-9;
+      }
+      std::string csv = path;
+      const size_t dot = csv.find_last_of('.');
+      if (dot != std::string::npos) csv.resize(dot);
+      std::ofstream m(csv + ".csv");
+      m.precision(12);
+      m << "metric,value\n"
+        << "l_comm_end," << end_role[ROLE_COMM] << "\n"
+        << "l_relay_end," << end_role[ROLE_RELAY] << "\n"
+        << "l_comp_end," << end_role[ROLE_COMP] << "\n"
+        << "l_reduce_end," << end_role[ROLE_REDUCE] << "\n"
+        << "first_comp_start," << first_comp << "\n";
+      for (int i = 0; i < 4; ++i) m << "busy_" << names[i] << "," << busy[i] << "\n";
+      m << "overlap_frac," << overlap << "\n";
+      m << "records," << n << "\n";
     }
   });
 }

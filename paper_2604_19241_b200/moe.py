@@ -61,6 +61,8 @@ _SIGS = {
     "eplab_export_layout": [_P, _P, _P],
     "eplab_timeline_enable": [_P, _I],
     "eplab_timeline_export": [_P, C.c_char_p, C.POINTER(C.c_double)],
+    "eplab_router_topk": [_P, _I, _I, _I, _I, _P, _P, _P],
+    "eplab_router_topk_bwd": [_P, _P, _P, _P, _I, _I, _I, _I, _P, _P],
 }
 
 
@@ -288,3 +290,54 @@ class EpMoEFunction(torch.autograd.Function):
         w_up, w_down = ctx.saved_tensors
         g = ctx.layer.backward(dy.contiguous(), w_up, w_down)
         return None, g["dx"], None, g["dgate"], g["dw_up"], g["dw_down"]
+
+
+def router_topk(logits, topk, renorm=True, stream=None):
+    """Router step in front of plan: fp32 logits [T][E] -> (topk_ids [T][k]
+    int32, gate_w [T][k] fp32) on device (eplab_router_topk; semantics in include/eplab_b200.h)."""
+    _need_cuda(logits, torch.float32)
+    T, E = logits.shape
+    ids = torch.empty(T, topk, dtype=torch.int32, device=logits.device)
+    gw = torch.empty(T, topk, dtype=torch.float32, device=logits.device)
+    st = stream if stream is not None else torch.cuda.current_stream(logits.device)
+    _check(lib().eplab_router_topk(logits.data_ptr(), T, E, topk, int(renorm), ids.data_ptr(), gw.data_ptr(),
+                                   st.cuda_stream))
+    return ids, gw
+
+
+def router_topk_bwd(logits, topk_ids, gate_w, dgate, renorm=True, stream=None):
+    """dgate [T][k] -> dlogits [T][E] (eplab_router_topk_bwd)."""
+    _need_cuda(logits, torch.float32)
+    T, E = logits.shape
+    dl = torch.empty(T, E, dtype=torch.float32, device=logits.device)
+    st = stream if stream is not None else torch.cuda.current_stream(logits.device)
+    _check(lib().eplab_router_topk_bwd(logits.data_ptr(), topk_ids.data_ptr(), gate_w.data_ptr(),
+                                       dgate.contiguous().data_ptr(), T, E, topk_ids.shape[1], int(renorm),
+                                       dl.data_ptr(), st.cuda_stream))
+    return dl
+
+
+def _need_cuda(t, dtype):
+    if not (t.is_cuda and t.dtype == dtype and t.is_contiguous() and t.dim() == 2):
+        raise EplabError(2, f"expected a contiguous 2-D {dtype} CUDA tensor, got {t.dtype} on {t.device}")
+
+
+class RouterFunction(torch.autograd.Function):
+    """Autograd wrapper: (topk_ids, gate_w) = router(logits); gradients flow from gate_w (e.g.
+    EpMoEFunction's dgate) back to the logits."""
+
+    @staticmethod
+    def forward(ctx, logits, topk, renorm=True):
+        logits = logits.contiguous()
+        ids, gw = router_topk(logits, topk, renorm)
+        ctx.renorm = renorm
+        ctx.save_for_backward(logits, ids, gw)
+        ctx.mark_non_differentiable(ids)
+        return ids, gw
+
+    @staticmethod
+    def backward(ctx, d_ids, d_gw):
+        logits, ids, gw = ctx.saved_tensors
+        if d_gw is None:
+            return None, None, None
+        return router_topk_bwd(logits, ids, gw, d_gw, ctx.renorm), None, None

@@ -262,3 +262,30 @@ def test_step_host_equals_device_path():
     assert (dg.numpy() == r["dgate"]).all()
     assert (to_u16(dwu) == r["dw_up"]).all() and (to_u16(dwd) == r["dw_down"]).all()
     L.close()
+
+
+def test_timeline_trace_and_metrics_csv(tmp_path):
+    """Device timeline -> Chrome trace + metric,value CSV (reference trace.cpp:36-66 layout)."""
+    import json
+    m = moe()
+    prob = Problem(1, 8, 2, 256, 512, 300, seed=4)
+    L = m.EpMoE(256, 512, 8, 2, 300)
+    L.timeline_enable(1 << 16)
+    ids = torch.from_numpy(prob.sel.reshape(300, 2).copy()).cuda()
+    gw = torch.from_numpy(prob.gw.reshape(300, 2).copy()).cuda()
+    L.forward(from_u16(prob.x[0]), ids, gw, from_u16(prob.w_up), from_u16(prob.w_down))
+    L.check()
+    path = str(tmp_path / "step.json")
+    ov = L.timeline_export(path)
+    assert 0.0 <= ov <= 1.0
+    ev = json.load(open(path))["traceEvents"]
+    cats = {e["cat"] for e in ev}
+    assert {"comm", "comp"} <= cats and all(e["dur"] >= 0 for e in ev)
+    rows = dict(line.strip().split(",") for line in open(tmp_path / "step.csv").readlines()[1:])
+    for key in ("l_comm_end", "l_comp_end", "first_comp_start", "busy_comm", "busy_comp",
+                "overlap_frac", "records"):
+        assert key in rows, key
+    assert int(rows["records"]) == len(ev)
+    assert float(rows["l_comp_end"]) >= float(rows["first_comp_start"]) >= 0.0
+    assert abs(float(rows["overlap_frac"]) - ov) < 1e-9
+    L.close()

@@ -6,6 +6,7 @@ Three anchors, per SURVEY.md §8(c):
   3. the committed fixtures in tests/golden/ (generated from (2) by tests/golden/make_golden.py),
      which travel to machines where /root/reference is absent.
 """
+import ctypes
 import os
 
 import numpy as np
@@ -316,3 +317,78 @@ def test_golden_fixtures():
     for r in range(world):
         s = ORC.send_schedule(tr, le, off, int(g["topk"]), world, epr, r)
         assert (s[0] == g[f"sched{r}_token"]).all() and (s[1] == g[f"sched{r}_slot"]).all()
+
+
+# ------------------------------------------------------------------ router (§8 f1)
+def _np_router(lg, k, renorm):
+    """Independent float64 restatement: stable top-k (descending, ties -> lower index) + softmax."""
+    lg = lg.astype(np.float64)
+    T, E = lg.shape
+    order = np.lexsort((np.broadcast_to(np.arange(E), lg.shape), -lg), axis=1)[:, :k]
+    sel = np.take_along_axis(lg, order, 1)
+    m = lg.max(1, keepdims=True)
+    num = np.exp(sel - m)
+    den = num.sum(1, keepdims=True) if renorm else np.exp(lg - m).sum(1, keepdims=True)
+    return order.astype(np.int32), num / den
+
+
+def _np_weights(lg, ids, renorm):
+    m = lg.max()
+    num = np.exp(lg[ids] - m)
+    return num / (num.sum() if renorm else np.exp(lg - m).sum())
+
+
+def test_router_exp_portable_accuracy():
+    o = po.Oracle()
+    o.lib.orc_exp_portable.restype = ctypes.c_float
+    o.lib.orc_exp_portable.argtypes = [ctypes.c_float]
+    xs = np.concatenate([np.linspace(-86.9, 0.0, 4001), -np.logspace(-8, 1.9, 500)]).astype(np.float32)
+    got = np.array([o.lib.orc_exp_portable(float(x)) for x in xs], np.float64)
+    ref = np.exp(xs.astype(np.float64))
+    assert (np.abs(got - ref) / ref).max() < 3e-7  # about 2.5 ulp
+    assert o.lib.orc_exp_portable(0.0) == 1.0 and o.lib.orc_exp_portable(-100.0) == 0.0
+
+
+@pytest.mark.parametrize("E,k,renorm", [(8, 2, True), (64, 8, True), (256, 8, False), (1000, 16, True),
+                                        (7, 7, False), (33, 1, True)])
+def test_router_oracle_vs_float64(E, k, renorm):
+    rng = np.random.default_rng(E * 31 + k)
+    lg = (rng.standard_normal((97, E)) * 3).astype(np.float32)
+    lg[5] = np.round(lg[5])          # many ties
+    lg[6] = 0.0                      # all equal: ids 0..k-1
+    ids, gw = po.Oracle().router_topk(lg, k, renorm)
+    rid, rgw = _np_router(lg, k, renorm)
+    assert (ids == rid).all()
+    assert (ids[6] == np.arange(k)).all()
+    assert np.abs(gw - rgw).max() <= 1e-6
+    if renorm:
+        assert np.abs(gw.astype(np.float64).sum(1) - 1).max() < 1e-5
+
+
+@pytest.mark.parametrize("renorm", [True, False])
+def test_router_bwd_oracle_vs_finite_differences(renorm):
+    rng = np.random.default_rng(5)
+    T, E, k = 6, 40, 4
+    lg = (rng.standard_normal((T, E)) * 2).astype(np.float32)
+    ids, gw = po.Oracle().router_topk(lg, k, renorm)
+    dg = rng.standard_normal((T, k)).astype(np.float32)
+    dl = po.Oracle().router_topk_bwd(lg, ids, gw, dg, renorm)
+    h = 1e-6
+    for t in range(T):
+        l64 = lg[t].astype(np.float64)
+        num = np.zeros(E)
+        for i in range(E):  # selection fixed (as in autograd through top-k)
+            a, b = l64.copy(), l64.copy()
+            a[i] += h
+            b[i] -= h
+            num[i] = (dg[t] @ _np_weights(a, ids[t], renorm) - dg[t] @ _np_weights(b, ids[t], renorm)) / (2 * h)
+        assert np.abs(dl[t] - num).max() < 1e-5, (t, np.abs(dl[t] - num).max())
+    if renorm:  # experts outside the selection get exactly zero
+        mask = np.ones((T, E), bool)
+        np.put_along_axis(mask, ids.astype(np.int64), False, 1)
+        assert (dl[mask] == 0).all()
+
+
+def test_router_validation():
+    with pytest.raises(ValueError):
+        po.Oracle().router_topk(np.zeros((2, 4), np.float32), 5)

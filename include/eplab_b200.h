@@ -158,13 +158,26 @@ EPLAB_API int eplab_moe_fwd(eplab_ctx* ctx, const int32_t* d_topk_ids, const flo
 EPLAB_API int eplab_moe_bwd(eplab_ctx* ctx, const void* d_dy, const void* d_w_up,
                             const void* d_w_down, void* d_dx, void* d_dw_up, void* d_dw_down,
                             float* d_dgate, void* stream);
-/* fwd+bwd with HOST routing/activations (pinned or pageable): H2D copies, the four
- * MegaKernels, D2H of y, dx and dgate, all on `stream`; synchronises before returning. */
+/* fwd+bwd with HOST routing/activations (pinned for asynchronous copies): H2D copies, the
+ * four MegaKernels on `stream`, D2H of y, dx and dgate. dY's upload runs under the forward
+ * MegaKernels and y's download under the backward ones (two copy streams). Synchronises before
+ * returning. */
 EPLAB_API int eplab_moe_step_host(eplab_ctx* ctx, const int32_t* h_topk_ids,
                                   const float* h_gate_w, int n_tok, const void* h_x,
                                   const void* h_dy, const void* d_w_up, const void* d_w_down,
                                   void* h_y, void* h_dx, float* h_dgate, void* d_dw_up,
                                   void* d_dw_down, void* stream);
+/* The same step enqueued without blocking the host. Consecutive steps alternate between two
+ * device staging sets, so step i+1's uploads overlap step i's MegaKernels and step i's
+ * downloads overlap step i+1's. Host inputs must stay unchanged and host outputs are valid only
+ * after eplab_host_join(ctx, s) + a synchronisation of s (or a later blocking step). */
+EPLAB_API int eplab_moe_step_host_async(eplab_ctx* ctx, const int32_t* h_topk_ids,
+                                        const float* h_gate_w, int n_tok, const void* h_x,
+                                        const void* h_dy, const void* d_w_up, const void* d_w_down,
+                                        void* h_y, void* h_dx, float* h_dgate, void* d_dw_up,
+                                        void* d_dw_down, void* stream);
+/* Makes `stream` wait (on the device) for every enqueued host-step copy. */
+EPLAB_API int eplab_host_join(eplab_ctx* ctx, void* stream);
 
 /* Synchronises `stream` and reports the device error word: 0 ok, 2 capacity exceeded,
  * 3 scoreboard watchdog fired (DeadlockError analogue, error.hpp:19-22). Clears it. */

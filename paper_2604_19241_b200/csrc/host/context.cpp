@@ -58,10 +58,13 @@ struct eplab_ctx {
   uint32_t* wg_cnt = nullptr;
   int* cursor = nullptr;
   int* err = nullptr;
-  // host-call staging (eplab_moe_step_host) and its copy stream / events
-  char* stage = nullptr;
-  cudaStream_t copy_st = nullptr;
-  cudaEvent_t ev_fwd = nullptr, ev_dy = nullptr, ev_y = nullptr;
+  // host-call staging (eplab_moe_step_host[_async]): two device buffer sets used by alternate
+  // steps, an H2D and a D2H copy stream, per-set events
+  char* stage[2] = {nullptr, nullptr};
+  size_t stage_bytes = 0;
+  uint64_t host_step = 0;
+  cudaStream_t h2d_st = nullptr, d2h_st = nullptr;
+  cudaEvent_t ev_in[2] = {}, ev_dy[2] = {}, ev_fwd[2] = {}, ev_bwd[2] = {}, ev_free[2] = {};
   // fixed tensor maps
   CUtensorMap tm_recv_x_k{}, tm_recv_x_mn{}, tm_hact_k{}, tm_recv_dy_k{}, tm_recv_dy_mn{},
       tm_hw_mn{}, tm_dgu_k{}, tm_dgu_mn{};
@@ -241,7 +244,8 @@ int eplab_init(const eplab_init_args* args, eplab_ctx** out) {
     c->cursor = reinterpret_cast<int*>(c->loc + o_cur);
     c->err = reinterpret_cast<int*>(c->loc + o_err);
 
-    // ---- host-call staging: ids, gate weights, x, dy, y, dx, dgate
+    // ---- host-call staging (allocated on the first host call): ids, gate weights, x, dy, y,
+    // dx, dgate
     o = 0;
     take(Tk * 4);
     take(Tk * 4);
@@ -250,7 +254,7 @@ int eplab_init(const eplab_init_args* args, eplab_ctx** out) {
     take((size_t)d.T_max * d.H * 2);
     take((size_t)d.T_max * d.H * 2);
     take(Tk * 4);
-    CK(cudaMalloc(&c->stage, o));
+    c->stage_bytes = o;
 
     // ---- fixed tensor maps
     using eplab_host::make_bf16_map;
@@ -279,12 +283,14 @@ int eplab_destroy(eplab_ctx* c) {
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   cudaFree(c->sym);
   cudaFree(c->loc);
-  cudaFree(c->stage);
-  if (c->copy_st) {
-    cudaStreamDestroy(c->copy_st);
-    cudaEventDestroy(c->ev_fwd);
-    cudaEventDestroy(c->ev_dy);
-    cudaEventDestroy(c->ev_y);
+  if (c->h2d_st) {
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(c->stage[b]);
+      for (cudaEvent_t e : {c->ev_in[b], c->ev_dy[b], c->ev_fwd[b], c->ev_bwd[b], c->ev_free[b]})
+        cudaEventDestroy(e);
+    }
+    cudaStreamDestroy(c->h2d_st);
+    cudaStreamDestroy(c->d2h_st);
   }
   if (c->tl_rec) cudaFree(c->tl_rec);
   if (c->tl_count) cudaFree(c->tl_count);
@@ -499,54 +505,94 @@ int eplab_moe_bwd(eplab_ctx* c, const void* dy, const void* w_up, const void* w_
   return rc;
 }
 
+namespace {
+
+// One layer step from host buffers, enqueued without blocking the host. Step i uses device
+// buffer set i % 2, so step i+1's uploads run under step i's MegaKernels:
+//   h2d stream : [wait free(b)] ids, gw, x -> in(b); dy -> dy(b)
+//   compute    : [wait in(b)] fwd -> fwd(b); [wait dy(b)] bwd -> bwd(b)
+//   d2h stream : [wait fwd(b)] y; [wait bwd(b)] dx, dgate -> free(b)
+// Only the first step's x upload and the last step's dx download are exposed in a stream of
+// steps. Host buffers should be pinned for the copies to be asynchronous.
+void step_host_enqueue(eplab_ctx* c, const int32_t* h_ids, const float* h_gw, int n_tok, const void* h_x,
+                       const void* h_dy, const void* w_up, const void* w_down, void* h_y, void* h_dx,
+                       float* h_dgate, void* dw_up, void* dw_down, cudaStream_t st) {
+  validate(n_tok >= 0 && n_tok <= c->d.T_max, "n_tok exceeds max_tokens");
+  CK(cudaSetDevice(c->device));
+  if (!c->h2d_st) {
+    CK(cudaStreamCreateWithFlags(&c->h2d_st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->d2h_st, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      CK(cudaMalloc(&c->stage[b], c->stage_bytes));
+      for (cudaEvent_t* e : {&c->ev_in[b], &c->ev_dy[b], &c->ev_fwd[b], &c->ev_bwd[b], &c->ev_free[b]})
+        CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+      CK(cudaEventRecord(c->ev_free[b], c->d2h_st));
+    }
+  }
+  const int b = (int)(c->host_step++ & 1);
+  const size_t Tk = (size_t)c->d.T_max * c->d.topk, TH = (size_t)c->d.T_max * c->d.H * 2;
+  char* s = c->stage[b];
+  int32_t* ids = reinterpret_cast<int32_t*>(s);
+  float* gw = reinterpret_cast<float*>(s + align_up(Tk * 4, 256));
+  char* x = s + 2 * align_up(Tk * 4, 256);
+  char* dy = x + align_up(TH, 256);
+  char* y = dy + align_up(TH, 256);
+  char* dx = y + align_up(TH, 256);
+  float* dg = reinterpret_cast<float*>(dx + align_up(TH, 256));
+  const size_t nk = (size_t)n_tok * c->d.topk, nh = (size_t)n_tok * c->d.H * 2;
+  CK(cudaStreamWaitEvent(c->h2d_st, c->ev_free[b], 0));
+  CK(cudaMemcpyAsync(ids, h_ids, nk * 4, cudaMemcpyHostToDevice, c->h2d_st));
+  CK(cudaMemcpyAsync(gw, h_gw, nk * 4, cudaMemcpyHostToDevice, c->h2d_st));
+  CK(cudaMemcpyAsync(x, h_x, nh, cudaMemcpyHostToDevice, c->h2d_st));
+  CK(cudaEventRecord(c->ev_in[b], c->h2d_st));
+  CK(cudaMemcpyAsync(dy, h_dy, nh, cudaMemcpyHostToDevice, c->h2d_st));
+  CK(cudaEventRecord(c->ev_dy[b], c->h2d_st));
+  CK(cudaStreamWaitEvent(st, c->ev_in[b], 0));
+  int r = eplab_moe_fwd(c, ids, gw, n_tok, x, w_up, w_down, y, st);
+  if (r) throw Fail{r, eplab_host::last_error()};
+  CK(cudaEventRecord(c->ev_fwd[b], st));
+  CK(cudaStreamWaitEvent(c->d2h_st, c->ev_fwd[b], 0));
+  CK(cudaMemcpyAsync(h_y, y, nh, cudaMemcpyDeviceToHost, c->d2h_st));
+  CK(cudaStreamWaitEvent(st, c->ev_dy[b], 0));
+  r = eplab_moe_bwd(c, dy, w_up, w_down, dx, dw_up, dw_down, dg, st);
+  if (r) throw Fail{r, eplab_host::last_error()};
+  CK(cudaEventRecord(c->ev_bwd[b], st));
+  CK(cudaStreamWaitEvent(c->d2h_st, c->ev_bwd[b], 0));
+  CK(cudaMemcpyAsync(h_dx, dx, nh, cudaMemcpyDeviceToHost, c->d2h_st));
+  CK(cudaMemcpyAsync(h_dgate, dg, nk * 4, cudaMemcpyDeviceToHost, c->d2h_st));
+  CK(cudaEventRecord(c->ev_free[b], c->d2h_st));
+}
+
+}  // namespace
+
 int eplab_moe_step_host(eplab_ctx* c, const int32_t* h_ids, const float* h_gw, int n_tok,
                         const void* h_x, const void* h_dy, const void* w_up, const void* w_down,
                         void* h_y, void* h_dx, float* h_dgate, void* dw_up, void* dw_down,
                         void* stream) {
-  // Copies overlap compute on a side stream: dY's H2D runs under the forward MegaKernels and
-  // y's D2H under the backward ones; only the routing/x upload and the dx/dgate download are
-  // exposed. Host buffers should be pinned for the copies to be asynchronous.
-  int rc = guarded([&] {
-    validate(n_tok >= 0 && n_tok <= c->d.T_max, "n_tok exceeds max_tokens");
-    CK(cudaSetDevice(c->device));
-    cudaStream_t st = (cudaStream_t)stream;
-    if (!c->copy_st) {
-      CK(cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking));
-      CK(cudaEventCreateWithFlags(&c->ev_fwd, cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&c->ev_dy, cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&c->ev_y, cudaEventDisableTiming));
-    }
-    const size_t Tk = (size_t)c->d.T_max * c->d.topk, TH = (size_t)c->d.T_max * c->d.H * 2;
-    char* s = c->stage;
-    int32_t* ids = reinterpret_cast<int32_t*>(s);
-    float* gw = reinterpret_cast<float*>(s + align_up(Tk * 4, 256));
-    char* x = s + 2 * align_up(Tk * 4, 256);
-    char* dy = x + align_up(TH, 256);
-    char* y = dy + align_up(TH, 256);
-    char* dx = y + align_up(TH, 256);
-    float* dg = reinterpret_cast<float*>(dx + align_up(TH, 256));
-    const size_t nk = (size_t)n_tok * c->d.topk, nh = (size_t)n_tok * c->d.H * 2;
-    CK(cudaMemcpyAsync(ids, h_ids, nk * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(gw, h_gw, nk * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(x, h_x, nh, cudaMemcpyHostToDevice, st));
-    CK(cudaEventRecord(c->ev_fwd, st));  // previous step's users of dy are ordered before this
-    CK(cudaStreamWaitEvent(c->copy_st, c->ev_fwd, 0));
-    CK(cudaMemcpyAsync(dy, h_dy, nh, cudaMemcpyHostToDevice, c->copy_st));
-    CK(cudaEventRecord(c->ev_dy, c->copy_st));
-    int r = eplab_moe_fwd(c, ids, gw, n_tok, x, w_up, w_down, y, stream);
-    if (r) throw Fail{r, eplab_host::last_error()};
-    CK(cudaEventRecord(c->ev_y, st));
-    CK(cudaStreamWaitEvent(c->copy_st, c->ev_y, 0));
-    CK(cudaMemcpyAsync(h_y, y, nh, cudaMemcpyDeviceToHost, c->copy_st));
-    CK(cudaStreamWaitEvent(st, c->ev_dy, 0));
-    r = eplab_moe_bwd(c, dy, w_up, w_down, dx, dw_up, dw_down, dg, stream);
-    if (r) throw Fail{r, eplab_host::last_error()};
-    CK(cudaMemcpyAsync(h_dx, dx, nh, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(h_dgate, dg, nk * 4, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(c->copy_st));
-    CK(cudaStreamSynchronize(st));
+  return guarded([&] {
+    step_host_enqueue(c, h_ids, h_gw, n_tok, h_x, h_dy, w_up, w_down, h_y, h_dx, h_dgate, dw_up, dw_down,
+                      (cudaStream_t)stream);
+    CK(cudaStreamSynchronize(c->d2h_st));
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
   });
-  return rc;
+}
+
+int eplab_moe_step_host_async(eplab_ctx* c, const int32_t* h_ids, const float* h_gw, int n_tok,
+                              const void* h_x, const void* h_dy, const void* w_up, const void* w_down,
+                              void* h_y, void* h_dx, float* h_dgate, void* dw_up, void* dw_down,
+                              void* stream) {
+  return guarded([&] {
+    step_host_enqueue(c, h_ids, h_gw, n_tok, h_x, h_dy, w_up, w_down, h_y, h_dx, h_dgate, dw_up, dw_down,
+                      (cudaStream_t)stream);
+  });
+}
+
+int eplab_host_join(eplab_ctx* c, void* stream) {
+  return guarded([&] {
+    if (!c->h2d_st) return;
+    CK(cudaSetDevice(c->device));
+    for (int b = 0; b < 2; ++b) CK(cudaStreamWaitEvent((cudaStream_t)stream, c->ev_free[b], 0));
+  });
 }
 
 int eplab_check(eplab_ctx* c, void* stream) {

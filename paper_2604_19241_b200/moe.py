@@ -55,6 +55,8 @@ _SIGS = {
     "eplab_moe_fwd": [_P, _P, _P, _I, _P, _P, _P, _P, _P],
     "eplab_moe_bwd": [_P, _P, _P, _P, _P, _P, _P, _P, _P],
     "eplab_moe_step_host": [_P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "eplab_moe_step_host_async": [_P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "eplab_host_join": [_P, _P],
     "eplab_check": [_P, _P],
     "eplab_export_token_map": [_P, _P, _P, _P, _P, _P],
     "eplab_export_schedule": [_P, _P, _P],
@@ -213,6 +215,17 @@ class EpMoE:
         _check(lib().eplab_moe_step_host(self.h, _ptr(ids_h), _ptr(gw_h), ids_h.shape[0], _ptr(x_h),
                                          _ptr(dy_h), _ptr(w_up), _ptr(w_down), _ptr(y_h), _ptr(dx_h),
                                          _ptr(dgate_h), _ptr(dw_up), _ptr(dw_down), _stream(stream)))
+
+    def step_host_async(self, ids_h, gw_h, x_h, dy_h, w_up, w_down, y_h, dx_h, dgate_h, dw_up, dw_down,
+                        stream=None):
+        """The same step enqueued without a host sync; consecutive steps overlap their copies with
+        each other's MegaKernels. Outputs are valid after host_join(stream) + stream sync."""
+        _check(lib().eplab_moe_step_host_async(self.h, _ptr(ids_h), _ptr(gw_h), ids_h.shape[0], _ptr(x_h),
+                                               _ptr(dy_h), _ptr(w_up), _ptr(w_down), _ptr(y_h), _ptr(dx_h),
+                                               _ptr(dgate_h), _ptr(dw_up), _ptr(dw_down), _stream(stream)))
+
+    def host_join(self, stream=None):
+        _check(lib().eplab_host_join(self.h, _stream(stream)))
 
     def check(self, stream=None):
         _check(lib().eplab_check(self.h, _stream(stream)))

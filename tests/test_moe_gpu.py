@@ -289,3 +289,33 @@ def test_timeline_trace_and_metrics_csv(tmp_path):
     assert float(rows["l_comp_end"]) >= float(rows["first_comp_start"]) >= 0.0
     assert abs(float(rows["overlap_frac"]) - ov) < 1e-9
     L.close()
+
+
+def test_step_host_async_pipelined_equals_blocking():
+    """Three back-to-back eplab_moe_step_host_async steps (alternating staging sets, copies
+    overlapping the neighbours' MegaKernels) give the blocking call's bits every step."""
+    prob = Problem(1, 8, 2, 256, 512, 200, seed=9)
+    ref, _, _ = run_layer(prob)
+    m = moe()
+    L = m.EpMoE(256, 512, 8, 2, 200)
+    ids = torch.from_numpy(prob.sel.reshape(200, 2).copy()).pin_memory()
+    gw = torch.from_numpy(prob.gw.reshape(200, 2).copy()).pin_memory()
+    x = from_u16(prob.x[0], "cpu").pin_memory()
+    dy = from_u16(prob.dy[0], "cpu").pin_memory()
+    wu, wd = from_u16(prob.w_up), from_u16(prob.w_down)
+    outs = [dict(y=torch.empty(200, 256, dtype=torch.bfloat16).pin_memory(),
+                 dx=torch.empty(200, 256, dtype=torch.bfloat16).pin_memory(),
+                 dg=torch.empty(200, 2, dtype=torch.float32).pin_memory()) for _ in range(3)]
+    dwu, dwd = torch.empty_like(wu), torch.empty_like(wd)
+    st = torch.cuda.current_stream()
+    for o in outs:
+        L.step_host_async(ids, gw, x, dy, wu, wd, o["y"], o["dx"], o["dg"], dwu, dwd)
+    L.host_join(st)
+    st.synchronize()
+    L.check()
+    r = ref[0][0]
+    for o in outs:
+        assert (to_u16(o["y"]) == r["y"]).all() and (to_u16(o["dx"]) == r["dx"]).all()
+        assert (o["dg"].numpy() == r["dgate"]).all()
+    assert (to_u16(dwu) == r["dw_up"]).all() and (to_u16(dwd) == r["dw_down"]).all()
+    L.close()

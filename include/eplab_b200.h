@@ -86,6 +86,12 @@ EPLAB_API int eplab_router_topk_bwd(const float* d_logits, const int32_t* d_topk
                                     float* d_dlogits, void* stream);
 
 
+/* ------------------------------------------- NB split-batch backward
+ * d_acc[i] = bf16_rne(float(d_acc[i]) + float(d_add[i])) for n bf16 elements (16-byte aligned):
+ * sums the per-sub-batch weight gradients of the opt-in non-bitwise split-batch backward
+ * (PAPER.md:647-651), the two-way split of precision.cpp:98-134 on real gradients. */
+EPLAB_API int eplab_bf16_accumulate(void* d_acc, const void* d_add, size_t n, void* stream);
+
 /* ------------------------------------------------------- EP-MoE context (per rank) */
 
 typedef struct eplab_ctx eplab_ctx;

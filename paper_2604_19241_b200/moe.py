@@ -57,6 +57,7 @@ _SIGS = {
     "eplab_moe_step_host": [_P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "eplab_moe_step_host_async": [_P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "eplab_host_join": [_P, _P],
+    "eplab_bf16_accumulate": [_P, _P, C.c_size_t, _P],
     "eplab_check": [_P, _P],
     "eplab_export_token_map": [_P, _P, _P, _P, _P, _P],
     "eplab_export_schedule": [_P, _P, _P],
@@ -200,6 +201,36 @@ class EpMoE:
         self._dispatch_bwd(dy, w_down, out, stream)
         self._combine_bwd(w_up, out, stream)
         return out
+
+    def step_split(self, x, topk_ids, gate_w, dy, w_up, w_down, n_sub=2, stream=None):
+        """Opt-in NON-BITWISE (NB) split-batch step: the
+        tokens are cut into n_sub contiguous sub-batches, each runs plan + the four MegaKernels,
+        and the weight gradients are summed in bf16 (eplab_bf16_accumulate). y, dx and dgate are
+        bitwise identical to the full-batch step (row-local); dw_up / dw_down differ by the
+        changed accumulation tree (the divergence precision.cpp:98-134 measures)."""
+        n = x.shape[0]
+        dev = self.device
+        y = torch.empty(n, self.H, dtype=torch.bfloat16, device=dev)
+        out = dict(dx=torch.empty(n, self.H, dtype=torch.bfloat16, device=dev),
+                   dw_up=torch.empty_like(w_up), dw_down=torch.empty_like(w_down),
+                   dgate=torch.empty(n, self.k, dtype=torch.float32, device=dev))
+        part = dict(dw_up=torch.empty_like(w_up), dw_down=torch.empty_like(w_down))
+        bounds = [n * i // n_sub for i in range(n_sub + 1)]
+        for i in range(n_sub):
+            lo, hi = bounds[i], bounds[i + 1]
+            self.plan(topk_ids[lo:hi], gate_w[lo:hi], stream)
+            self.dispatch_group_gemm(x[lo:hi], w_up, stream)
+            self.group_gemm_combine(w_down, y[lo:hi], stream)
+            o = dict(dx=out["dx"][lo:hi], dgate=out["dgate"][lo:hi],
+                     dw_up=out["dw_up"] if i == 0 else part["dw_up"],
+                     dw_down=out["dw_down"] if i == 0 else part["dw_down"])
+            self._dispatch_bwd(dy[lo:hi], w_down, o, stream)
+            self._combine_bwd(w_up, o, stream)
+            if i:
+                for key in ("dw_up", "dw_down"):
+                    _check(lib().eplab_bf16_accumulate(_ptr(out[key]), _ptr(part[key]), out[key].numel(),
+                                                       _stream(stream)))
+        return y, out
 
     def _dispatch_bwd(self, dy, w_down, out, stream=None):
         _check(lib().eplab_dispatch_group_gemm_bwd(self.h, _ptr(dy), _ptr(w_down), _ptr(out["dw_down"]),

@@ -319,3 +319,29 @@ def test_step_host_async_pipelined_equals_blocking():
         assert (o["dg"].numpy() == r["dgate"]).all()
     assert (to_u16(dwu) == r["dw_up"]).all() and (to_u16(dwd) == r["dw_down"]).all()
     L.close()
+
+
+def test_nb_split_batch_variant_divergence():
+    """Opt-in NB split-batch step (§8 f3): y/dx/dgate bitwise equal to the full-batch (BW) step,
+    weight gradients within the oracle tolerance but no longer bitwise equal (the accumulation
+    tree changed, precision.cpp:98-134)."""
+    prob = Problem(1, 8, 2, 256, 512, 1000, seed=12)
+    ref, _, _ = run_layer(prob)
+    r = ref[0][0]
+    m = moe()
+    L = m.EpMoE(256, 512, 8, 2, 1000)
+    ids = torch.from_numpy(prob.sel.reshape(1000, 2).copy()).cuda()
+    gw = torch.from_numpy(prob.gw.reshape(1000, 2).copy()).cuda()
+    y, g = L.step_split(from_u16(prob.x[0]), ids, gw, from_u16(prob.dy[0]), from_u16(prob.w_up),
+                        from_u16(prob.w_down), n_sub=2)
+    L.check()
+    assert (to_u16(y) == r["y"]).all() and (to_u16(g["dx"]) == r["dx"]).all()
+    assert (g["dgate"].cpu().numpy() == r["dgate"]).all()
+    o = prob.oracle()
+    diff = 0
+    for key in ("dw_up", "dw_down"):
+        nb = to_u16(g[key])
+        assert_close(bf16_to_f32(nb).reshape(-1), bf16_to_f32(o[key]).reshape(-1), key)
+        diff += int((nb != r[key]).sum())
+    assert diff > 0  # the split changes some weight-gradient bits
+    L.close()

@@ -4,7 +4,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libeplab_b200.so")
+LIB_PATH = os.environ.get("EPLAB_LIB") or os.path.join(_HERE, "libeplab_b200.so")  # EPLAB_LIB: A/B experiments
 _lib = None
 
 

@@ -136,6 +136,7 @@ MkArgs base_args(eplab_ctx* c) {
   a.tl = Timeline{c->tl_rec, c->tl_count, c->tl_cap};
   a.dbg = getenv("EPLAB_DBG") ? atoi(getenv("EPLAB_DBG")) : 0;
   a.pair = c->pair;
+  a.comm_bulk = getenv("EPLAB_COMM") && std::string(getenv("EPLAB_COMM")) == "bulk";
   return a;
 }
 

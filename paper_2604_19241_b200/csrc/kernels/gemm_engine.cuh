@@ -200,8 +200,11 @@ __device__ __forceinline__ void gemm_teardown(GemmSmem* S) {
 }
 
 // Row-chunk helpers used by epilogues: 32 fp32 accumulators of one row.
+// tcgen05.ld / wait::ld are .sync.aligned: the warp must be converged, which the divergent
+// per-row code (live rows, predicated loads) around the call sites does not guarantee by itself.
 __device__ __forceinline__ void acc_chunk(uint32_t taddr, int chunk, float (&v)[32]) {
   uint32_t r[32];
+  __syncwarp();
   tmem_ld32(taddr + chunk * 32, r);
   tmem_ld_wait();
 #pragma unroll

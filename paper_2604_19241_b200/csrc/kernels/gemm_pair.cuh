@@ -62,7 +62,8 @@ __device__ __forceinline__ void gemm_teardown_pair(GemmSmem* S) {
 template <class Mode>
 __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& tm,
                                 uint8_t* tiles_smem, GemmSmem* S, int tile_lo, int tile_hi,
-                                int* __restrict__ cursor, const Timeline& tl, uint32_t rank) {
+                                int* __restrict__ cursor, const Timeline& tl, uint32_t rank,
+                                const Watchdog& wd = Watchdog{}) {
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = lane_id();
   uint8_t* sA = tiles_smem;
@@ -97,7 +98,7 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
           td = Mode::tile_pair(args, id - tile_lo);
           Mode::before_loads_pair(args, td);
         }
-        mbar_wait_cluster(&S->rempty[slot], ((it / RING) & 1) ^ 1);
+        mbar_wait_cluster_wd(&S->rempty[slot], ((it / RING) & 1) ^ 1, wd, 40);
         const int rv = is_tile ? id - tile_lo : TASK_STOP;
         S->ring[slot] = rv;
         S->ring_td[slot] = td;
@@ -122,7 +123,7 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
       uint32_t stage = 0, phase = 0;
       for (int it = 0;; ++it) {
         const int slot = it % RING;
-        mbar_wait_cluster(&S->rfull[slot], (it / RING) & 1);
+        mbar_wait_cluster_wd(&S->rfull[slot], (it / RING) & 1, wd, 41);
         const int t = S->ring[slot];
         const TileDesc td = S->ring_td[slot];
         mbar_arrive_cluster(rempty0 + slot * 8);
@@ -130,7 +131,7 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
         fence_proxy_async_global();
         if (leader) S->tstart[it & 7] = globaltimer();
         for (int kb = 0; kb < td.nkb; ++kb) {
-          mbar_wait(&S->empty[stage], phase ^ 1);
+          mbar_wait_wd(&S->empty[stage], phase ^ 1, wd, 42);
           const uint32_t full0 = mapa_shared(smem_u32(&S->full[stage]), 0);
           if (leader)
             mbar_arrive_expect_tx(&S->full[stage], 2 * P_STAGE_BYTES);
@@ -152,7 +153,7 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
       uint32_t stage = 0, phase = 0;
       for (int it = 0;; ++it) {
         const int slot = it % RING;
-        mbar_wait_cluster(&S->rfull[slot], (it / RING) & 1);
+        mbar_wait_cluster_wd(&S->rfull[slot], (it / RING) & 1, wd, 43);
         const int t = S->ring[slot];
         const TileDesc td = S->ring_td[slot];
         mbar_arrive(&S->rempty[slot]);
@@ -160,11 +161,11 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
         const int amn = Mode::a_mn(td), bmn = Mode::b_mn(td);
         const uint32_t idesc = make_idesc(2 * BM, BN, amn, bmn);
         const uint32_t acc = it & 1;
-        mbar_wait_cluster(&S->tempty[acc], ((it >> 1) & 1) ^ 1);
+        mbar_wait_cluster_wd(&S->tempty[acc], ((it >> 1) & 1) ^ 1, wd, 44);
         tc_fence_after();
         const uint32_t d = S->tmem_base + acc * BN;
         for (int kb = 0; kb < td.nkb; ++kb) {
-          mbar_wait(&S->full[stage], phase);
+          mbar_wait_wd(&S->full[stage], phase, wd, 45);
           tc_fence_after();
           const uint32_t as = a0 + stage * P_HALF_BYTES;
           const uint32_t bs = b0 + stage * P_HALF_BYTES;
@@ -193,7 +194,7 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
     const uint32_t tempty0 = mapa_shared(smem_u32(&S->tempty[0]), 0);
     for (int it = 0;; ++it) {
       const int slot = it % RING;
-      mbar_wait_cluster(&S->rfull[slot], (it / RING) & 1);
+      mbar_wait_cluster_wd(&S->rfull[slot], (it / RING) & 1, wd, 46);
       const int t = S->ring[slot];
       const TileDesc td = S->ring_td[slot];
       __syncwarp();
@@ -206,7 +207,7 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
       const bool work = Mode::half_has_work(half);
       if (work) Mode::epilogue_prefetch(args, half, r);
       const uint32_t acc = it & 1;
-      mbar_wait(&S->tfull[acc], (it >> 1) & 1);
+      mbar_wait_wd(&S->tfull[acc], (it >> 1) & 1, wd, 47);
       tc_fence_after();
       const uint32_t taddr = S->tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
       if (work) Mode::epilogue(args, tm, half, taddr, r, tiles_smem + TILES_BYTES + q * EPI_WARP_BYTES);

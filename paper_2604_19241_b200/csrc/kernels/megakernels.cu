@@ -342,6 +342,94 @@ __device__ void comm_pipeline(const MkArgs& a, int ph, GemmSmem* S, uint8_t* sbu
   S->cphase[iss] = par;
 }
 
+// Comm role data mover (default): warp copies. Warp w moves the copied items [32w, 32w+32) of
+// the round with 16-byte loads/stores, two rows in flight per warp (16 x 16 B per lane), and in
+// the backward phase folds the gate gradient <dY_t, o_{t,j}> of each item while the dY row is in
+// registers (tools/bulk_copy_probe.cu: 38-43 GB/s per CTA vs 26-45 for the bulk-copy engine
+// with 64 CTAs). The warp then releases its items: one system-scope fence, then relaxed rowgroup
+// counter updates aggregated per counter (relay off) or per-slot flags (relay on).
+__device__ void comm_warp_copy(const MkArgs& a, int ph, GemmSmem* S, int cnt) {
+  const Dims& d = a.d;
+  const int k = d.topk, vecs = d.H / 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q0 = warp * 32, q1 = min(cnt, q0 + 32);
+  const int4* src_base = reinterpret_cast<const int4*>(ph == 0 ? a.x : a.dy);
+  auto dst_row = [&](int q) {
+    const SymPtrs& P = a.peers.p[S->cdst[q]];
+    return reinterpret_cast<int4*>(ph == 0 ? P.recv_x : P.recv_dy) + (size_t)S->cslot[q] * vecs;
+  };
+  if (ph == 0) {
+    int q = q0;
+    while (true) {
+      while (q < q1 && S->cdst[q] < 0) ++q;
+      if (q >= q1) break;
+      int qb = q + 1;
+      while (qb < q1 && S->cdst[qb] < 0) ++qb;
+      const bool two = qb < q1;
+      const int4* sa = src_base + (size_t)(S->citem[q] / k) * vecs;
+      const int4* sb = src_base + (size_t)(S->citem[two ? qb : q] / k) * vecs;
+      int4* da = dst_row(q);
+      int4* db = dst_row(two ? qb : q);
+      for (int c = lane; c < vecs; c += 256) {
+        int4 va[8], vb[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (c + 32 * u < vecs) {
+            va[u] = ld_nc_v4(sa + c + 32 * u);
+            if (two) vb[u] = ld_nc_v4(sb + c + 32 * u);
+          }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (c + 32 * u < vecs) {
+            da[c + 32 * u] = va[u];
+            if (two) db[c + 32 * u] = vb[u];
+          }
+      }
+      q = two ? qb + 1 : q1;
+    }
+  } else {
+    const int4* orow_base = reinterpret_cast<const int4*>(a.peers.p[d.rank].rep);
+    for (int q = q0; q < q1; ++q) {
+      const int i = S->citem[q];
+      const bool copy = S->cdst[q] >= 0;
+      const int4* src = src_base + (size_t)(i / k) * vecs;
+      const int4* orow = orow_base + (size_t)i * vecs;
+      int4* dst = copy ? dst_row(q) : nullptr;
+      float gacc = 0.f;
+      for (int c = lane; c < vecs; c += 256) {
+        int4 v[8], o[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (c + 32 * u < vecs) {
+            v[u] = ld_nc_v4(src + c + 32 * u);
+            o[u] = ld_nc_v4(orow + c + 32 * u);
+          }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (c + 32 * u < vecs) {
+            if (copy) dst[c + 32 * u] = v[u];
+            gacc = dot8_bf16(v[u], o[u], gacc);
+          }
+      }
+#pragma unroll
+      for (int s2 = 16; s2 > 0; s2 >>= 1) gacc += __shfl_xor_sync(0xffffffffu, gacc, s2);
+      if (lane == 0) a.dgate[i] = gacc;
+    }
+  }
+  // release this warp's copied items (fence + relaxed updates)
+  __syncwarp();
+  fence_acq_rel_sys();
+  const int q = q0 + lane;
+  const bool mine = q < q1 && S->cdst[q] >= 0;
+  if (a.n_relay > 0) {
+    if (mine) st_relaxed_sys(a.peers.p[S->cdst[q]].slot_flag + S->cslot[q], a.epoch * 2 + ph);
+  } else {
+    uint32_t* ctr = mine ? rg_counter(a.peers.p[S->cdst[q]], d, ph, a.par, S->cslot[q] >> 7) : nullptr;
+    const unsigned m = __match_any_sync(0xffffffffu, (unsigned long long)ctr);
+    if (ctr && lane == __ffs(m) - 1) red_relaxed_sys_add(ctr, (uint32_t)__popc(m));
+  }
+}
+
 __device__ void comm_task(const MkArgs& a, int task, int ph, GemmSmem* S, uint8_t* sbuf) {
   const Dims& d = a.d;
   const int k = d.topk, H = d.H, me = d.rank;
@@ -381,6 +469,13 @@ __device__ void comm_task(const MkArgs& a, int task, int ph, GemmSmem* S, uint8_
       S->cdst[threadIdx.x] = prim_slot >= 0 ? -1 : dst;
     }
     __syncthreads();
+    if (!a.comm_bulk) {
+      comm_warp_copy(a, ph, S, cnt);
+      __syncthreads();
+      continue;
+    }
+    // bulk-copy engine mover (EPLAB_COMM=bulk; the round-1 default, kept for comparison:
+    // 436 / 747 us vs 386 / 645 us for the Qwen3 fwd / bwd comm tasks, profiles/r01_comm_movers.txt)
     const int n_iss = H <= 4096 ? 4 : 2;  // 14 KB rows: 2 issuers x 6 slots
     if (warp < n_iss) {  // issuer warps
       if (lane == 0) {
@@ -459,39 +554,45 @@ __device__ void relay_task(const MkArgs& a, int task, int ph) {
 // ------------------------------------------------------------------ reduce role
 // Top-k completeness barrier, then the fixed k-ascending fold (
 // precision.cpp:31-37 order): forward y = bf16(fma-fold of w_j * o_j), backward
-// dx = bf16(sum_j dX_j), both in fp32.
-__device__ void reduce_task(const MkArgs& a, int task, int ph) {
+// dx = bf16(sum_j dX_j), both in fp32. A token's k replica rows are one contiguous block
+// [t*k, t*k+k) x H; each lane keeps KT x U 16-byte loads in flight (KT >= k replicas x U column
+// chunks, 16 per lane) so the HBM-bound fold is not latency-bound.
+template <int KT>
+__device__ __forceinline__ void reduce_tokens(const MkArgs& a, int ph, long long t0, long long t1) {
+  constexpr int U = 16 / KT;
   const Dims& d = a.d;
-  const int k = d.topk, H = d.H;
+  const int k = d.topk, vecs = d.H / 8;
   const SymPtrs& me = a.peers.p[d.rank];
-  long long t0, t1;
-  even_slice(a.p.n_tok, a.n_red, task, t0, t1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t need = (uint32_t)(k * (H / BN));
-  const __nv_bfloat16* rep = ph == 0 ? me.rep : me.rep_dx;
-  __nv_bfloat16* out = ph == 0 ? a.y : a.dx;
+  const uint32_t need = (uint32_t)(k * (d.H / BN));
+  const int4* rep = reinterpret_cast<const int4*>(ph == 0 ? me.rep : me.rep_dx);
+  int4* out = reinterpret_cast<int4*>(ph == 0 ? a.y : a.dx);
   for (long long t = t0 + warp; t < t1; t += GEMM_THREADS / 32) {
     if (lane == 0)
       wait_geq_sys(tok_counter(me, d, ph, a.par, (int)t), need, a.timeout_ns, a.err, 20 + ph, (int)t);
     __syncwarp();
-    float w[16];
-    for (int j = 0; j < k; ++j) w[j] = ph == 0 ? a.p.gate_w[t * k + j] : 1.0f;
-    for (int c0 = lane * 8; c0 < H; c0 += 4 * 256) {
-      float acc[4][8];
+    float w[KT];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+    for (int j = 0; j < KT; ++j) w[j] = (j < k && ph == 0) ? a.p.gate_w[t * k + j] : 1.0f;
+    const int4* base = rep + (size_t)t * k * vecs;
+    for (int c = lane; c < vecs; c += 32 * U) {
+      int4 v[KT][U];
+#pragma unroll
+      for (int j = 0; j < KT; ++j)
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (j < k && c + 32 * u < vecs) v[j][u] = base[(size_t)j * vecs + c + 32 * u];
+      float acc[U][8];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc[u][q] = 0.f;
-      for (int j = 0; j < k; ++j) {
-        int4 v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (c0 + u * 256 < H)
-            v[u] = *reinterpret_cast<const int4*>(rep + ((size_t)t * k + j) * H + c0 + u * 256);
+      for (int j = 0; j < KT; ++j) {
+        if (j >= k) break;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (c0 + u * 256 >= H) continue;
-          const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
+        for (int u = 0; u < U; ++u) {
+          const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&v[j][u]);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const float2 f = __bfloat1622float2(hv[q]);
@@ -506,17 +607,29 @@ __device__ void reduce_task(const MkArgs& a, int task, int ph) {
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (c0 + u * 256 >= H) continue;
+      for (int u = 0; u < U; ++u) {
+        if (c + 32 * u >= vecs) continue;
         int4 o;
         o.x = (int)pack_bf16(acc[u][0], acc[u][1]);
         o.y = (int)pack_bf16(acc[u][2], acc[u][3]);
         o.z = (int)pack_bf16(acc[u][4], acc[u][5]);
         o.w = (int)pack_bf16(acc[u][6], acc[u][7]);
-        *reinterpret_cast<int4*>(out + (size_t)t * H + c0 + u * 256) = o;
+        out[(size_t)t * vecs + c + 32 * u] = o;
       }
     }
   }
+}
+
+__device__ void reduce_task(const MkArgs& a, int task, int ph) {
+  long long t0, t1;
+  even_slice(a.p.n_tok, a.n_red, task, t0, t1);
+  const int k = a.d.topk;
+  if (k <= 4)
+    reduce_tokens<4>(a, ph, t0, t1);
+  else if (k <= 8)
+    reduce_tokens<8>(a, ph, t0, t1);
+  else
+    reduce_tokens<16>(a, ph, t0, t1);
 }
 
 // ------------------------------------------------------------------ GEMM modes
@@ -797,8 +910,9 @@ struct ModeDgradDown {
     const int4* gsrc = reinterpret_cast<const int4*>(a.gu + m * 2 * F + td.n0);
     const int4* usrc = reinterpret_cast<const int4*>(a.gu + m * 2 * F + F + td.n0);
     // saved g, u of chunk c+1 are in flight while chunk c is computed (software pipelining)
-    int4 gq[4], uq[4];
-    if (live) {
+    int4 gq[4] = {}, uq[4] = {};
+    const bool ld_gu = live && !(a.dbg & 16);  // experiment: dbg 16 skips the saved g, u loads
+    if (ld_gu) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         gq[i] = gsrc[i];
@@ -810,7 +924,7 @@ struct ModeDgradDown {
       float v[32];
       acc_chunk(taddr, c, v);
       int4 gn[4], un[4];
-      if (live && c + 1 < BN / 32) {
+      if (ld_gu && c + 1 < BN / 32) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           gn[i] = gsrc[(c + 1) * 4 + i];
@@ -860,7 +974,7 @@ struct ModeDgradDown {
         tma_store_2d(&tm.m[5], stg + 2 * EPI_TILE_BYTES, f0, row0);  // HW
         tma_store_commit();
       }
-      if (live && c + 1 < BN / 32) {
+      if (ld_gu && c + 1 < BN / 32) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           gq[i] = gn[i];
@@ -1086,7 +1200,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // pair up: the leader learns both CTAs' first non-pre ids
   if (threadIdx.x == 0) st_cluster_u32(mapa_shared(smem_u32(&S->pend[rank]), 0), (uint32_t)id);
   cluster_sync_all();
-  gemm_roles_pair<Mode>(a, tm, base, S, n_pre, n_pre + n_tiles, a.cursor, a.tl, rank);
+  gemm_roles_pair<Mode>(a, tm, base, S, n_pre, n_pre + n_tiles, a.cursor, a.tl, rank,
+                        Watchdog{});  // Watchdog{a.err, a.timeout_ns} to debug engine hangs
   cluster_sync_all();
   if (threadIdx.x == 0) {
     const int pn = (int)ld_cluster_u32(mapa_shared(smem_u32(&S->post_n), 0));

@@ -133,8 +133,10 @@ struct MkArgs {
   int n_disp, n_relay, n_red;
   unsigned long long timeout_ns;
   Timeline tl;
-  int dbg;  // debug bits (experiments only): 1 = skip epilogue stores of the up GEMM
+  int dbg;  // debug bits (experiments only): 2/4 = skip dgrad epilogue TMA stores / staging,
+            // 16 = skip the saved g, u loads of the dgrad epilogue
   int pair;  // 1: CTA-pair (cta_group::2) engine
+  int comm_bulk;  // 1: comm role moves rows with the TMA bulk-copy engine (EPLAB_COMM=bulk)
 };
 
 }  // namespace eplab_dev

@@ -286,6 +286,52 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
   while (!mbar_try_wait_cluster(bar, parity)) {
   }
 }
+
+// Watchdog for the engine's mbarrier waits: a wait that exceeds `timeout` ns records
+// (3, site, parity, -1, where) in err[0..4] (first failure wins, eplab_check reports it) and
+// returns; once err[0] is set every later watched wait returns at once. err == nullptr: no
+// watchdog (plain GEMMs).
+struct Watchdog {
+  int* err = nullptr;
+  unsigned long long timeout = 0;
+};
+__device__ __forceinline__ bool wd_expired(const Watchdog& wd, unsigned long long t0, int site,
+                                           uint32_t parity) {
+  uint64_t now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+  if (now - t0 <= wd.timeout) return *reinterpret_cast<const volatile int*>(wd.err) != 0 && now - t0 > 1000000;
+  if (atomicCAS(wd.err, 0, 3) == 0) {
+    wd.err[1] = site;
+    wd.err[2] = (int)parity;
+    wd.err[3] = -1;
+    wd.err[4] = (int)(blockIdx.x * 256 + threadIdx.x);
+  }
+  return true;
+}
+__device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, const Watchdog& wd,
+                                             int site) {
+  if (mbar_try_wait(bar, parity) || !wd.err) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+    return;
+  }
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (uint32_t n = 1; !mbar_try_wait(bar, parity); ++n)
+    if ((n & 255) == 0 && wd_expired(wd, t0, site, parity)) return;
+}
+__device__ __forceinline__ void mbar_wait_cluster_wd(uint64_t* bar, uint32_t parity, const Watchdog& wd,
+                                                     int site) {
+  if (mbar_try_wait_cluster(bar, parity) || !wd.err) {
+    while (!mbar_try_wait_cluster(bar, parity)) {
+    }
+    return;
+  }
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (uint32_t n = 1; !mbar_try_wait_cluster(bar, parity); ++n)
+    if ((n & 255) == 0 && wd_expired(wd, t0, site, parity)) return;
+}
 __device__ __forceinline__ void st_cluster_u32(uint32_t cluster_addr, uint32_t v) {
   asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
 }

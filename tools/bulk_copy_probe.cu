@@ -43,6 +43,26 @@ __global__ void __launch_bounds__(256, 1) probe(const int4* src, int4* dst, cons
     }
     return;
   }
+  if (variant == 4) {  // warp copies, two rows per warp in flight (16 x 16 B per lane)
+    const int vecs = row_bytes / 16;
+    for (int r = lo + warp * 2; r < hi; r += 16) {
+      const bool two = r + 1 < hi;
+      const int4* s0 = src + (size_t)perm[r] * vecs;
+      const int4* s1 = src + (size_t)perm[two ? r + 1 : r] * vecs;
+      int4* d0 = dst + (size_t)r * vecs;
+      int4* d1 = dst + (size_t)(two ? r + 1 : r) * vecs;
+      for (int c = lane; c < vecs; c += 256) {
+        int4 v[8], w[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (c + u * 32 < vecs) { v[u] = ld_nc_v4(s0 + c + u * 32); w[u] = ld_nc_v4(s1 + c + u * 32); }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (c + u * 32 < vecs) { d0[c + u * 32] = v[u]; if (two) d1[c + u * 32] = w[u]; }
+      }
+    }
+    return;
+  }
   const int iss = variant == 2 ? ISS : 1;
   if (warp >= iss || lane != 0) return;
   constexpr int NS = NSLOT;  // slots owned by this issuer
@@ -106,7 +126,7 @@ int main() {
              row_bytes, grid, variant, ms, n / ms / 1e6, n / ms / 1e6 / grid,
              cudaGetErrorString(cudaGetLastError()));
     };
-    for (int grid : {32, 148}) {
+    for (int grid : {32, 64, 148}) {
       if (row_bytes <= 4096) {
         run(probe<48, 4>, grid, 0);
         run(probe<48, 4>, grid, 1);
@@ -121,6 +141,7 @@ int main() {
         run(probe<12, 4>, grid, 2);
       }
       run(probe<12, 4>, grid, 3);
+      run(probe<12, 4>, grid, 4);
     }
     cudaFree(src);
     cudaFree(dst);

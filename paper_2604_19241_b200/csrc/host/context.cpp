@@ -129,7 +129,7 @@ MkArgs base_args(eplab_ctx* c) {
   a.err = c->err;
   a.epoch = c->epoch;
   a.par = (int)(c->epoch & 1);
-  a.n_disp = std::max(1, c->cfg.n_disp);
+  a.n_disp = std::max(0, c->cfg.n_disp);
   a.n_relay = std::max(0, c->cfg.n_relay);
   a.n_red = std::max(1, c->cfg.n_red);
   a.timeout_ns = c->timeout_ns;
@@ -137,6 +137,10 @@ MkArgs base_args(eplab_ctx* c) {
   a.dbg = getenv("EPLAB_DBG") ? atoi(getenv("EPLAB_DBG")) : 0;
   a.pair = c->pair;
   a.comm_bulk = getenv("EPLAB_COMM") && std::string(getenv("EPLAB_COMM")) == "bulk";
+  a.comm_cursor = c->cursor + 2;
+  a.spare_warps = getenv("EPLAB_SPARE") ? atoi(getenv("EPLAB_SPARE")) : 1;
+  // somebody must move the rows: the bulk mover and spare-less pools need >= 1 comm CTA
+  if (a.n_disp == 0 && (a.comm_bulk || !a.spare_warps)) a.n_disp = 1;
   return a;
 }
 
@@ -352,7 +356,7 @@ int eplab_connect_local(eplab_ctx* const* ctxs, int n) {
 int eplab_set_tune_config(eplab_ctx* c, const eplab_tune_config* cfg) {
   return guarded([&] {
     validate(cfg->w == 8 || cfg->w == 16 || cfg->w == 32, "w must be one of {8,16,32}");
-    validate(cfg->n_disp >= 1, "n_disp must be >= 1");
+    validate(cfg->n_disp >= 0, "n_disp must be >= 0 (0: the GEMM CTAs' spare warps move the rows)");
     validate(cfg->n_relay >= 0, "n_relay must be >= 0");
     // deadlock constraint of types.cpp:59-64; producers are claimed first, so the persistent
     // grid (one CTA per SM) always keeps at least one SM for compute.

@@ -5,7 +5,20 @@
 #include "gemm_core.cuh"
 #include "moe_common.cuh"
 
+#include <type_traits>
+
 namespace eplab_dev {
+
+// A Mode with `static constexpr bool SPARE = true` gives the engine's otherwise idle warps work
+// through `Mode::spare(args, timeline)` (the MegaKernels' comm warp split).
+template <class M, class = void>
+struct has_spare : std::false_type {};
+template <class M>
+struct has_spare<M, std::void_t<decltype(M::SPARE)>> : std::bool_constant<M::SPARE> {};
+template <class Mode, class Args, class TL>
+__device__ __forceinline__ void call_spare(const Args& a, const TL& tl) {
+  if constexpr (has_spare<Mode>::value) Mode::spare(a, tl);
+}
 
 __device__ __forceinline__ void timeline_push(const Timeline& tl, unsigned long long t0,
                                               unsigned long long t1, uint32_t role, int task) {
@@ -36,7 +49,9 @@ __device__ int gemm_roles(const typename Mode::Args& args, const TmaSet& tm, uin
   uint8_t* sA = tiles_smem;
   uint8_t* sB = tiles_smem + STAGES * A_STAGE_BYTES;
 
-  if (warp == 3) {
+  if (has_spare<Mode>::value && warp == 2) {
+    call_spare<Mode>(args, tl);  // the TMEM owner is idle between allocation and teardown
+  } else if (warp == 3) {
     // ---------------- scheduler: claims tile ids, decodes them and resolves their scoreboard
     // dependencies (Mode::before_loads) ahead of the producer; stops at the first non-tile id
     if (lane == 0) {

@@ -70,7 +70,12 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
   uint8_t* sB = tiles_smem + P_STAGES * P_HALF_BYTES;
   const bool leader = rank == 0;
 
-  if (warp == 3) {
+  // spare warps: warp 2 (TMEM owner, idle between allocation and teardown) of both CTAs and the
+  // non-leader's warps 1 and 3 (the leader alone issues MMAs and schedules)
+  const bool spare = warp == 2 || (!leader && (warp == 1 || warp == 3));
+  if (has_spare<Mode>::value && spare) {
+    call_spare<Mode>(args, tl);
+  } else if (warp == 3) {
     if (leader && lane == 0) {
       // ---------------- scheduler (leader)
       int np = 0;

@@ -342,34 +342,64 @@ __device__ void comm_pipeline(const MkArgs& a, int ph, GemmSmem* S, uint8_t* sbu
   S->cphase[iss] = par;
 }
 
-// Comm role data mover (default): warp copies. Warp w moves the copied items [32w, 32w+32) of
-// the round with 16-byte loads/stores, two rows in flight per warp (16 x 16 B per lane), and in
-// the backward phase folds the gate gradient <dY_t, o_{t,j}> of each item while the dY row is in
-// registers (tools/bulk_copy_probe.cu: 38-43 GB/s per CTA vs 26-45 for the bulk-copy engine
-// with 64 CTAs). The warp then releases its items: one system-scope fence, then relaxed rowgroup
-// counter updates aggregated per counter (relay off) or per-slot flags (relay on).
-__device__ void comm_warp_copy(const MkArgs& a, int ph, GemmSmem* S, int cnt) {
+// Comm role (default mover): a pool of 32-item rounds of the priority-ordered send schedule
+// (token_map.cpp:108-126), claimed in order from one atomic round counter by every comm
+// worker -- the 8 warps of each comm CTA (SM split, n_disp) and the spare warps of the GEMM
+// CTAs (warp split: warp 2 of both CTAs of a pair, warps 1 and 3 of the non-leader CTA). A
+// warp moves its round with 16-byte loads/stores, two rows in flight (16 x 16 B per lane); in
+// the backward phase it folds the gate gradient <dY_t, o_{t,j}> of every item while the dY row
+// is in registers. Then it releases the round: one system-scope fence, relaxed rowgroup
+// counter updates aggregated per counter (relay off) or per-slot epoch flags (relay on).
+__device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
   const Dims& d = a.d;
-  const int k = d.topk, vecs = d.H / 8;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int q0 = warp * 32, q1 = min(cnt, q0 + 32);
+  const int k = d.topk, vecs = d.H / 8, me = d.rank;
+  const int lane = threadIdx.x & 31;
+  const long long n = (long long)a.p.n_tok * k;
+  const long long idx = r * 32 + lane;
+  int item = -1, slot = 0, dst = -1;  // dst < 0: the row does not travel from here
+  if (idx < n) {
+    const int i = a.p.sched[idx];
+    const int t = i / k;
+    const int e = a.p.topk_ids[i];
+    const int dr = e / d.epr, el = e - dr * d.epr;
+    slot = a.p.dst_slot[i];
+    int prim_j = -1, best = el;
+    if (a.n_relay > 0)  // relay on: the first (token, dst) replica in priority order travels
+      for (int jj = 0; jj < k; ++jj) {
+        const int e2 = a.p.topk_ids[t * k + jj];
+        if (e2 / d.epr == dr && e2 - dr * d.epr < best) {
+          best = e2 - dr * d.epr;
+          prim_j = jj;
+        }
+      }
+    const SymPtrs& P = a.peers.p[dr];
+    const int prim_slot = prim_j >= 0 ? a.p.dst_slot[t * k + prim_j] : -1;
+    if (ph == 0) P.meta[slot] = SlotMeta{me, i, a.p.gate_w[i], prim_slot};
+    // a duplicate's flag means "metadata valid"; the relay copies it after the primary's flag
+    if (prim_slot >= 0) st_release_sys(P.slot_flag + slot, a.epoch * 2 + ph);
+    item = i;
+    dst = prim_slot >= 0 ? -1 : dr;
+  }
   const int4* src_base = reinterpret_cast<const int4*>(ph == 0 ? a.x : a.dy);
-  auto dst_row = [&](int q) {
-    const SymPtrs& P = a.peers.p[S->cdst[q]];
-    return reinterpret_cast<int4*>(ph == 0 ? P.recv_x : P.recv_dy) + (size_t)S->cslot[q] * vecs;
+  auto dst_row = [&](int dr, int sl) {
+    const SymPtrs& P = a.peers.p[dr];
+    return reinterpret_cast<int4*>(ph == 0 ? P.recv_x : P.recv_dy) + (size_t)sl * vecs;
   };
   if (ph == 0) {
-    int q = q0;
-    while (true) {
-      while (q < q1 && S->cdst[q] < 0) ++q;
-      if (q >= q1) break;
-      int qb = q + 1;
-      while (qb < q1 && S->cdst[qb] < 0) ++qb;
-      const bool two = qb < q1;
-      const int4* sa = src_base + (size_t)(S->citem[q] / k) * vecs;
-      const int4* sb = src_base + (size_t)(S->citem[two ? qb : q] / k) * vecs;
-      int4* da = dst_row(q);
-      int4* db = dst_row(two ? qb : q);
+    unsigned m = __ballot_sync(0xffffffffu, dst >= 0);
+    while (m) {
+      const int qa = __ffs(m) - 1;
+      m &= m - 1;
+      const int qb = m ? __ffs(m) - 1 : qa;
+      if (m) m &= m - 1;
+      const bool two = qb != qa;
+      const int ia = __shfl_sync(0xffffffffu, item, qa), ib = __shfl_sync(0xffffffffu, item, qb);
+      const int sa_ = __shfl_sync(0xffffffffu, slot, qa), sb_ = __shfl_sync(0xffffffffu, slot, qb);
+      const int da_ = __shfl_sync(0xffffffffu, dst, qa), db_ = __shfl_sync(0xffffffffu, dst, qb);
+      const int4* sa = src_base + (size_t)(ia / k) * vecs;
+      const int4* sb = src_base + (size_t)(ib / k) * vecs;
+      int4* da = dst_row(da_, sa_);
+      int4* db = dst_row(db_, sb_);
       for (int c = lane; c < vecs; c += 256) {
         int4 va[8], vb[8];
 #pragma unroll
@@ -385,16 +415,18 @@ __device__ void comm_warp_copy(const MkArgs& a, int ph, GemmSmem* S, int cnt) {
             if (two) db[c + 32 * u] = vb[u];
           }
       }
-      q = two ? qb + 1 : q1;
     }
   } else {
-    const int4* orow_base = reinterpret_cast<const int4*>(a.peers.p[d.rank].rep);
-    for (int q = q0; q < q1; ++q) {
-      const int i = S->citem[q];
-      const bool copy = S->cdst[q] >= 0;
+    const int4* orow_base = reinterpret_cast<const int4*>(a.peers.p[me].rep);
+    unsigned m = __ballot_sync(0xffffffffu, item >= 0);
+    while (m) {
+      const int q = __ffs(m) - 1;
+      m &= m - 1;
+      const int i = __shfl_sync(0xffffffffu, item, q);
+      const int dq = __shfl_sync(0xffffffffu, dst, q), sq = __shfl_sync(0xffffffffu, slot, q);
       const int4* src = src_base + (size_t)(i / k) * vecs;
       const int4* orow = orow_base + (size_t)i * vecs;
-      int4* dst = copy ? dst_row(q) : nullptr;
+      int4* drow = dq >= 0 ? dst_row(dq, sq) : nullptr;
       float gacc = 0.f;
       for (int c = lane; c < vecs; c += 256) {
         int4 v[8], o[8];
@@ -407,7 +439,7 @@ __device__ void comm_warp_copy(const MkArgs& a, int ph, GemmSmem* S, int cnt) {
 #pragma unroll
         for (int u = 0; u < 8; ++u)
           if (c + 32 * u < vecs) {
-            if (copy) dst[c + 32 * u] = v[u];
+            if (drow) drow[c + 32 * u] = v[u];
             gacc = dot8_bf16(v[u], o[u], gacc);
           }
       }
@@ -416,21 +448,39 @@ __device__ void comm_warp_copy(const MkArgs& a, int ph, GemmSmem* S, int cnt) {
       if (lane == 0) a.dgate[i] = gacc;
     }
   }
-  // release this warp's copied items (fence + relaxed updates)
+  // release the round's copied rows (fence + relaxed updates)
   __syncwarp();
   fence_acq_rel_sys();
-  const int q = q0 + lane;
-  const bool mine = q < q1 && S->cdst[q] >= 0;
   if (a.n_relay > 0) {
-    if (mine) st_relaxed_sys(a.peers.p[S->cdst[q]].slot_flag + S->cslot[q], a.epoch * 2 + ph);
+    if (dst >= 0) st_relaxed_sys(a.peers.p[dst].slot_flag + slot, a.epoch * 2 + ph);
   } else {
-    uint32_t* ctr = mine ? rg_counter(a.peers.p[S->cdst[q]], d, ph, a.par, S->cslot[q] >> 7) : nullptr;
-    const unsigned m = __match_any_sync(0xffffffffu, (unsigned long long)ctr);
-    if (ctr && lane == __ffs(m) - 1) red_relaxed_sys_add(ctr, (uint32_t)__popc(m));
+    uint32_t* ctr = dst >= 0 ? rg_counter(a.peers.p[dst], d, ph, a.par, slot >> 7) : nullptr;
+    const unsigned mm = __match_any_sync(0xffffffffu, (unsigned long long)ctr);
+    if (ctr && lane == __ffs(mm) - 1) red_relaxed_sys_add(ctr, (uint32_t)__popc(mm));
   }
 }
 
+// A comm worker warp: claim rounds until the pool is empty. Returns the number of rounds moved.
+__device__ int comm_rounds(const MkArgs& a, int ph) {
+  const long long n_rounds = ((long long)a.p.n_tok * a.d.topk + 31) / 32;
+  const int lane = threadIdx.x & 31;
+  int done = 0;
+  for (;;) {
+    long long r = 0;
+    if (lane == 0) r = atomicAdd(reinterpret_cast<unsigned long long*>(a.comm_cursor), 1ull);
+    r = __shfl_sync(0xffffffffu, r, 0);
+    if (r >= n_rounds) break;
+    comm_round_warp(a, ph, r);
+    ++done;
+  }
+  return done;
+}
+
 __device__ void comm_task(const MkArgs& a, int task, int ph, GemmSmem* S, uint8_t* sbuf) {
+  if (!a.comm_bulk) {  // every warp of the comm CTA drains the round pool
+    comm_rounds(a, ph);
+    return;
+  }
   const Dims& d = a.d;
   const int k = d.topk, H = d.H, me = d.rank;
   const long long n = (long long)a.p.n_tok * k;
@@ -469,11 +519,6 @@ __device__ void comm_task(const MkArgs& a, int task, int ph, GemmSmem* S, uint8_
       S->cdst[threadIdx.x] = prim_slot >= 0 ? -1 : dst;
     }
     __syncthreads();
-    if (!a.comm_bulk) {
-      comm_warp_copy(a, ph, S, cnt);
-      __syncthreads();
-      continue;
-    }
     // bulk-copy engine mover (EPLAB_COMM=bulk; the round-1 default, kept for comparison:
     // 436 / 747 us vs 386 / 645 us for the Qwen3 fwd / bwd comm tasks, profiles/r01_comm_movers.txt)
     const int n_iss = H <= 4096 ? 4 : 2;  // 14 KB rows: 2 issuers x 6 slots
@@ -637,9 +682,20 @@ __device__ void reduce_task(const MkArgs& a, int task, int ph) {
 
 // Forward up projection: A = recv_x (K-major over H), B = W_up gate rows [f0,f0+128) and up
 // rows [F+f0, ..) (K-major). Epilogue: GU (bf16) and h = bf16(silu(g) * u) from the bf16 g, u.
+// Spare warps of the dispatch MegaKernels' GEMM CTAs drain the comm pool too (warp split);
+// their activity goes into the device timeline as one comm interval per warp.
+__device__ __forceinline__ void spare_comm(const MkArgs& a, const Timeline& tl, int ph) {
+  if (!a.spare_warps || a.comm_bulk) return;
+  const unsigned long long t0 = globaltimer();
+  const int n = comm_rounds(a, ph);
+  if (n > 0 && (threadIdx.x & 31) == 0) timeline_push(tl, t0, globaltimer(), ROLE_COMM, -1 - (int)(threadIdx.x >> 5));
+}
+
 struct ModeUp {
   using Args = MkArgs;
   static constexpr bool HAS_TILE_DONE = false;
+  static constexpr bool SPARE = true;
+  __device__ static void spare(const Args& a, const Timeline& tl) { spare_comm(a, tl, 0); }
   __device__ static int a_mn(const TileDesc&) { return 0; }
   __device__ static int b_mn(const TileDesc&) { return 0; }
   __device__ static TileDesc tile(const Args& a, int t) {
@@ -812,6 +868,8 @@ __device__ __forceinline__ void wgrad_store(const CUtensorMap* map, const TileDe
 struct ModeDgradDown {
   using Args = MkArgs;
   static constexpr bool HAS_TILE_DONE = true;
+  static constexpr bool SPARE = true;
+  __device__ static void spare(const Args& a, const Timeline& tl) { spare_comm(a, tl, 1); }
   __device__ static int n_dgrad_pair(const Args& a) { return a.p.mpair_pre[a.d.epr] * (a.d.F / BN); }
   __device__ static TileDesc tile_pair(const Args& a, int t) {
     const int nd = n_dgrad_pair(a);
@@ -1229,7 +1287,7 @@ using namespace eplab_dev;
 template <int KIND, class Mode>
 static int launch_mk(const TmaSet& tm, const MkArgs& a, int grid, cudaStream_t st) {
   static bool attr = false, attr_p = false;
-  cudaMemsetAsync(a.cursor, 0, sizeof(int), st);
+  cudaMemsetAsync(a.cursor, 0, 16, st);  // task cursor + comm round counter
   if (!a.pair) {
     auto fn = megakernel<KIND, Mode>;
     if (!attr) {

@@ -136,6 +136,8 @@ struct MkArgs {
   int dbg;  // debug bits (experiments only): 2/4 = skip dgrad epilogue TMA stores / staging,
             // 16 = skip the saved g, u loads of the dgrad epilogue
   int pair;  // 1: CTA-pair (cta_group::2) engine
+  int* comm_cursor;  // [2] u64 round counter of the comm pool (zeroed per launch with cursor)
+  int spare_warps;  // 1: the GEMM CTAs' spare warps join the comm pool (warp split)
   int comm_bulk;  // 1: comm role moves rows with the TMA bulk-copy engine (EPLAB_COMM=bulk)
 };
 

@@ -110,10 +110,12 @@ def choose_config(H, F, E, k, tokens, world, n_sm=148):
     """TuneConfig for one layer shape from the B200 model (n_red = all SMs; w = 8)."""
     best, _, _ = search_layer(shape(H, F, E, k, tokens), hw(world, n_sm=n_sm))
     best.n_red = n_sm
-    # Measured floor (profiles/r01_ndisp_sweep.txt): the model does not yet capture the start-up of
-    # the GEMM tiles behind the first landed rowgroups, and at EP=1 the measured optimum is >= 64
-    # comm CTAs for all three BASELINE shapes. (EP>1: same floor, not yet measured on NVLink.)
-    floor = (64 * n_sm) // 148
+    # Measured floor: the model does not yet capture the start-up of the GEMM tiles behind the
+    # first landed rowgroups. With the GEMM CTAs' spare warps in the comm pool (default), 16 comm
+    # CTAs is the measured optimum at EP=1 (profiles/r01_spare_warps.txt); without them (round-1
+    # kernels, EPLAB_SPARE=0) it was >= 64 (profiles/r01_ndisp_sweep.txt). EP>1: not yet measured.
+    import os
+    floor = ((16 if os.environ.get("EPLAB_SPARE", "1") != "0" else 64) * n_sm) // 148
     if best.n_disp < floor and floor + best.n_relay < n_sm:
         best.n_disp = floor
     return best

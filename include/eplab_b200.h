@@ -129,6 +129,11 @@ EPLAB_API int eplab_connect_local(eplab_ctx* const* ctxs, int n);
 
 EPLAB_API int eplab_set_tune_config(eplab_ctx* ctx, const eplab_tune_config* cfg);
 EPLAB_API int eplab_get_tune_config(const eplab_ctx* ctx, eplab_tune_config* cfg);
+/* Comm-pool workers of the dispatch MegaKernels (the unified primitive's warp split): with
+ * spare_warps = 1 (default) the GEMM CTAs' idle warps drain the same priority-ordered round pool
+ * as the n_disp comm CTAs, so n_disp may be 0; bulk_mover = 1 moves rows through the TMA
+ * bulk-copy engine (comm CTAs only) instead of warp copies. Results are bitwise identical. */
+EPLAB_API int eplab_set_comm_options(eplab_ctx* ctx, int spare_warps, int bulk_mover);
 /* Persistent grid size (default: all SMs). Several ranks sharing one GPU (the single-device
  * multi-rank test mode) each get a disjoint budget so their MegaKernels are co-resident. */
 EPLAB_API int eplab_set_sm_budget(eplab_ctx* ctx, int n_sm);

@@ -74,6 +74,9 @@ struct eplab_ctx {
   bool planned = false;
   eplab_tune_config cfg{32, 0, 0, 148, 8};
   int pair = 1;  // CTA-pair engine (EPLAB_ENGINE=single selects the single-CTA one)
+  // comm pool workers: spare GEMM warps join (warp split; EPLAB_SPARE=0 disables), bulk-copy
+  // mover instead of warp copies (EPLAB_COMM=bulk); eplab_set_comm_options overrides both
+  int spare_warps = 1, comm_bulk = 0;
   // timeline
   TimelineRec* tl_rec = nullptr;
   int* tl_count = nullptr;
@@ -136,9 +139,12 @@ MkArgs base_args(eplab_ctx* c) {
   a.tl = Timeline{c->tl_rec, c->tl_count, c->tl_cap};
   a.dbg = getenv("EPLAB_DBG") ? atoi(getenv("EPLAB_DBG")) : 0;
   a.pair = c->pair;
-  a.comm_bulk = getenv("EPLAB_COMM") && std::string(getenv("EPLAB_COMM")) == "bulk";
+  a.comm_bulk = c->comm_bulk;
   a.comm_cursor = c->cursor + 2;
-  a.spare_warps = getenv("EPLAB_SPARE") ? atoi(getenv("EPLAB_SPARE")) : 1;
+  a.spare_warps = c->spare_warps;
+  // A/B experiments: environment switches read per launch
+  if (const char* e = getenv("EPLAB_COMM")) a.comm_bulk = std::string(e) == "bulk";
+  if (const char* e = getenv("EPLAB_SPARE")) a.spare_warps = atoi(e);
   // somebody must move the rows: the bulk mover and spare-less pools need >= 1 comm CTA
   if (a.n_disp == 0 && (a.comm_bulk || !a.spare_warps)) a.n_disp = 1;
   return a;
@@ -378,6 +384,15 @@ int eplab_set_sm_budget(eplab_ctx* c, int n_sm) {
       c->cfg.n_disp = std::max(1, n_sm / 4);
       c->cfg.n_relay = c->cfg.n_relay ? 1 : 0;
     }
+  });
+}
+
+int eplab_set_comm_options(eplab_ctx* c, int spare_warps, int bulk_mover) {
+  return guarded([&] {
+    validate(spare_warps == 0 || spare_warps == 1, "spare_warps must be 0 or 1");
+    validate(bulk_mover == 0 || bulk_mover == 1, "bulk_mover must be 0 or 1");
+    c->spare_warps = spare_warps;
+    c->comm_bulk = bulk_mover;
   });
 }
 

@@ -47,6 +47,7 @@ _SIGS = {
     "eplab_set_tune_config": [_P, C.POINTER(TuneConfig)],
     "eplab_get_tune_config": [_P, C.POINTER(TuneConfig)],
     "eplab_set_sm_budget": [_P, _I],
+    "eplab_set_comm_options": [_P, _I, _I],
     "eplab_plan": [_P, _P, _P, _I, _P],
     "eplab_dispatch_group_gemm": [_P, _P, _P, _P],
     "eplab_group_gemm_combine": [_P, _P, _P, _P],
@@ -160,6 +161,9 @@ class EpMoE:
         if isinstance(cfg, (tuple, list)):
             cfg = TuneConfig(*cfg)
         _check(lib().eplab_set_tune_config(self.h, C.byref(cfg)))
+
+    def set_comm_options(self, spare_warps=True, bulk_mover=False):
+        _check(lib().eplab_set_comm_options(self.h, int(spare_warps), int(bulk_mover)))
 
     def tune_config(self):
         c = TuneConfig()

@@ -62,7 +62,7 @@ class Problem:
                                      self.w_up, self.w_down, self.dy)
 
 
-def run_layer(prob, world=None, cfg=None, reps=1):
+def run_layer(prob, world=None, cfg=None, reps=1, comm=None):
     """Runs fwd+bwd on `world` virtual ranks sharing cuda:0 (each with its own SM budget and
     stream). Returns per-rank outputs as numpy (bf16 as uint16)."""
     m = moe()
@@ -82,6 +82,9 @@ def run_layer(prob, world=None, cfg=None, reps=1):
     if cfg is not None:
         for r in ranks:
             r.set_tune_config(cfg)
+    if comm is not None:
+        for r in ranks:
+            r.set_comm_options(*comm)
     streams = [torch.cuda.Stream() for _ in range(W)]
     ins = []
     for r in range(W):
@@ -151,6 +154,27 @@ def test_layer_deterministic_and_relay_invariant():
     for key in ("y", "dx", "dgate", "dw_up", "dw_down"):
         assert (a[0][0][key] == a[1][0][key]).all(), f"run-to-run {key}"
         assert (a[0][0][key] == b[0][0][key]).all(), f"relay vs alltoall {key}"
+
+
+def test_comm_workers_bitwise_invariant():
+    """The comm pool's workers (SM split n_disp, warp split = the GEMM CTAs' spare warps) and the
+    row mover (warp copies / TMA bulk copies) change who moves which row, never the result."""
+    prob = Problem(1, 16, 4, 512, 256, 300, seed=9)
+    ref, _, _ = run_layer(prob, cfg=(16, 0, 1, 64, 8))                        # default pool
+    variants = [dict(cfg=(0, 0, 1, 64, 8)),                                    # spare warps only
+                dict(cfg=(8, 0, 1, 64, 8), comm=(0, 0)),                       # comm CTAs only
+                dict(cfg=(8, 0, 1, 64, 8), comm=(0, 1)),                       # bulk-copy mover
+                dict(cfg=(0, 2, 1, 64, 8))]                                    # relay + spare warps
+    for v in variants:
+        got, _, _ = run_layer(prob, **v)
+        for key in ("y", "dx", "dgate", "dw_up", "dw_down"):
+            assert (ref[0][0][key] == got[0][0][key]).all(), f"{v}: {key}"
+    check_vs_oracle(prob, gather(ref[0]))
+    relay2, _, _ = run_layer(Problem(2, 16, 4, 256, 256, 192, seed=5), cfg=(0, 4, 1, 64, 8))
+    a2a2, _, _ = run_layer(Problem(2, 16, 4, 256, 256, 192, seed=5), cfg=(4, 0, 1, 64, 8), comm=(0, 0))
+    ga, gb = gather(relay2[0]), gather(a2a2[0])
+    for key in ("y", "dx", "dgate", "dw_up", "dw_down"):
+        assert (ga[key] == gb[key]).all(), f"EP=2 relay+spare vs comm CTAs: {key}"
 
 
 def test_token_map_bit_exact_vs_reference_fixture_ep2():

@@ -112,6 +112,23 @@ def dist_info():
     return rank, world, local
 
 
+def hbm_bytes_per_step(cfg_name, world):
+    """Algorithmic HBM bytes of one fwd+bwd step on one GPU (balanced routing): every tensor of
+    the layer read or written once per use: the dispatch copies, both GEMMs' operands
+    and outputs, the saved activations, replica slots, the reductions, the weight gradients."""
+    H, F, E, k, T = CONFIGS[cfg_name]
+    R = T * k                      # rows received per GPU (balanced)
+    El = E // world
+    row = 2 * H
+    w_up, w_down = El * 2 * F * H * 2, El * H * F * 2
+    fwd_d = T * row + R * row + R * row + w_up + R * 2 * F * 2 + R * F * 2
+    fwd_c = R * F * 2 + w_down + R * row + T * k * row + T * row
+    bwd_d = T * row + R * row + T * k * row + R * row + w_down + R * 2 * F * 2 + R * 2 * F * 2 + R * F * 2 \
+        + R * row + R * F * 2 + w_down
+    bwd_c = R * 4 * F + w_up + R * row + R * 4 * F + R * row + w_up + T * k * row + T * row
+    return float(fwd_d + fwd_c + bwd_d + bwd_c)
+
+
 def algorithmic(cfg_name, world):
     """fwd+bwd FLOPs per token (18 k H F) and NVLink bytes per token per GPU."""
     H, F, E, k, T = CONFIGS[cfg_name]
@@ -146,15 +163,23 @@ def cpu_layer_sample(cfg_name, n_tok, threads, seed=7):
 
 
 def cpu_baseline(cfg_name, budget_s=12.0):
+    """The CPU port timed on two bounded samples (n1 < n2 tokens). A layer fwd+bwd has a per-token
+    cost and a per-step cost independent of the token count (writing every expert's weight
+    gradient), so the two samples give t(n) = a + b*n; `value` is the workload's T tokens over
+    a + b*T (both terms measured, the T-token step itself is not run)."""
+    T = CONFIGS[cfg_name][4]
     threads = os.cpu_count() or 1
-    n = 2
-    dt = cpu_layer_sample(cfg_name, n, threads)
-    while dt < budget_s / 4 and n < 4096:
-        n *= 2
-        dt = cpu_layer_sample(cfg_name, n, threads)
-    return {"value": n / dt, "unit": "tokens/s", "cores": threads, "kind": "port",
-            "sample": f"{n} tokens of the {cfg_name} layer fwd+bwd (EP=1, all {CONFIGS[cfg_name][2]} experts) "
-                      f"through the C oracle (oracle/eplab_oracle.c, OpenMP), {dt:.2f} s"}
+    n1 = 2
+    t1 = cpu_layer_sample(cfg_name, n1, threads)
+    n2 = n1 + 8  # a few s of per-token work on top of the per-step cost
+    t2 = cpu_layer_sample(cfg_name, n2, threads)
+    b = max((t2 - t1) / (n2 - n1), 1e-9)
+    a = max(t1 - b * n1, 0.0)
+    return {"value": T / (a + b * T), "unit": "tokens/s", "cores": threads, "kind": "port",
+            "per_token_s": b, "per_step_s": a,
+            "sample": f"{n1} and {n2} tokens of the {cfg_name} layer fwd+bwd (EP=1, all {CONFIGS[cfg_name][2]} "
+                      f"experts) through the C oracle (oracle/eplab_oracle.c, OpenMP): {t1:.2f} s and {t2:.2f} s "
+                      f"-> t(n) = {a:.2f} s + {b * 1e3:.1f} ms * n, value = {T} / t({T})"}
 
 
 def run_unfused(args):
@@ -409,6 +434,7 @@ def run_ours(args):
         t_gemm = flops_tok * T / (peak_sust * 1e12)
         t_nvl = nvl_tok * T / (NVL_GBS * 1e9)
         roof_ms = max(t_gemm, t_nvl) * 1e3
+        t_hbm = hbm_bytes_per_step(args.config, world) / (hbm * 1e9)
         cpu = cpu_baseline(args.config) if not args.no_cpu_baseline else None
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -432,8 +458,11 @@ def run_ours(args):
                          "peak_source": f"{peak_src} bf16 sustained (kernel timed inside the step)",
                          "frac_of_burst": ach / peak_burst},
             "roofline_step": {"roofline_ms": roof_ms, "frac": roof_ms / ms, "t_gemm_ms": t_gemm * 1e3,
-                              "t_nvlink_ms": t_nvl * 1e3,
-                              "note": "max(18kHF*T / sustained bf16 peak, NVLink bytes / 770 GB/s)"},
+                              "t_nvlink_ms": t_nvl * 1e3, "t_hbm_ms": t_hbm * 1e3,
+                              "hbm_bytes": hbm_bytes_per_step(args.config, world),
+                              "note": "roofline_ms = max(18kHF*T / sustained bf16 peak, NVLink bytes / 770 GB/s) "
+                                      "(the north-star definition); t_hbm_ms = algorithmic HBM bytes of the step / "
+                                      "measured HBM bandwidth, a second bound that the tensor and HBM traffic share"},
             "kernel_ms": kms,
             "overlap": {"fraction": overlap,
                         "definition": "time with >=1 comm/relay task AND >=1 GEMM tile active / time with "

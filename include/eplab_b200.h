@@ -235,7 +235,8 @@ typedef struct {
   double w_gap, w_red, w_rem;
 } eplab_breakdown;                   /* LatencyBreakdown, perf_model.hpp:17-35 */
 typedef struct {
-  double mu, tile_overhead, comm_bw_per_sm, relay_bw_per_sm, reduce_bw, launch, epi_bw_per_sm;
+  double mu, tile_overhead, comm_bw_per_sm, relay_bw_per_sm, reduce_bw, launch, epi_bw_per_sm,
+      spare_sm_equiv, hbm_overlap;
 } eplab_b200_calib;                  /* B200 calibration of this build's MegaKernels */
 typedef struct {
   double fwd_dispatch, fwd_combine, bwd_dispatch, bwd_combine, total, t_gemm_bound, t_nvl_bound;

@@ -454,34 +454,50 @@ LayerPrediction predict_layer(const MoEShape& m, const HardwareSpec& s, const Tu
   const double nvl_rows = relay ? T * (W - 1) * q : rows * (double)(W - 1) / W;
   const double k_rem = m.topk * (double)(W - 1) / W;
   const double dup_rows = relay ? std::max(0.0, rows - sent_rows) : 0.0;
-  const double l_comm = std::max(sent_rows * S / (c.n_disp * k.comm_bw_per_sm),
+  // comm capacity: n_disp comm CTAs plus the GEMM CTAs' spare warps (the warp split), both
+  // draining one round pool; only the comm CTAs' time is taken from the GEMM
+  const double comm_units = std::max(c.n_disp + k.spare_sm_equiv, 1e-3);
+  const double l_comm = std::max(sent_rows * S / (comm_units * k.comm_bw_per_sm),
                                  W > 1 ? nvl_rows * S / s.bw_nvl : 0.0);
   const double l_relay = relay ? dup_rows * S / (c.n_relay * k.relay_bw_per_sm) : 0.0;
   const double l_push = W > 1 ? T * k_rem * S / s.bw_nvl : 0.0;
   const double l_reduce = T * (m.topk + 1) * S / k.reduce_bw;
   // persistent grid: SM-seconds spread over n_sm, but never less than whole waves of the
   // kernel's dominant tile (quantisation matters for small batches)
+  // algorithmic HBM bytes per kernel: every tensor read or written once per use (the dispatch
+  // copies, both GEMMs' operands and outputs, saved activations, replica slots, reductions, dW)
+  const double w_up = epr * 2 * F * H * 2, w_down = epr * H * F * 2;
+  const double b_fd = T * S + rows * S + rows * S + w_up + rows * 2 * F * 2 + rows * F * 2;
+  const double b_fc = rows * F * 2 + w_down + rows * S + T * m.topk * S + T * S;
+  const double b_bd = T * S + rows * S + T * m.topk * S + rows * S + w_down + rows * 4 * F * 2 +
+                      rows * F * 2 + rows * S + rows * F * 2 + w_down;
+  const double b_bc = rows * 4 * F + w_up + rows * S + rows * 4 * F + rows * S + w_up + T * m.topk * S + T * S;
+  // persistent grid: SM-seconds spread over n_sm, but never less than whole waves of the
+  // kernel's dominant tile (quantisation matters for small batches); the HBM traffic overlaps
+  // the compute only partly (hbm_overlap)
   auto kernel = [&](double sm_seconds, double critical, double extra, double tiles = 0,
-                    double t_one = 0) {
+                    double t_one = 0, double hbm_bytes = 0) {
     const double waves = tiles > 0 ? std::ceil(tiles / s.n_sm) * t_one : 0.0;
-    return std::max({sm_seconds / s.n_sm, critical, waves}) + extra + k.launch;
+    const double comp = std::max({sm_seconds / s.n_sm, critical, waves});
+    const double mem = hbm_bytes / s.bw_hbm;
+    return std::max(comp, mem) + k.hbm_overlap * std::min(comp, mem) + extra + k.launch;
   };
   const double n_pre_sm = c.n_disp * l_comm + c.n_relay * l_relay;
   // forward
   const double up = mblocks * (F / 128) * tile_t(H, kEpiUp);
   p.fwd_dispatch = kernel(up + n_pre_sm, std::max(l_comm, l_relay) + tile_t(H, kEpiUp), 0.0,
-                          mblocks * (F / 128), tile_t(H, kEpiUp));
+                          mblocks * (F / 128), tile_t(H, kEpiUp), b_fd);
   const double down = mblocks * (H / 256) * tile_t(F, kEpiPush);
-  p.fwd_combine = kernel(down, l_push, l_reduce, mblocks * (H / 256), tile_t(F, kEpiPush));
+  p.fwd_combine = kernel(down, l_push, l_reduce, mblocks * (H / 256), tile_t(F, kEpiPush), b_fc);
   // backward (dY dispatch also folds the gate gradient: + k*S of replica reads per token)
-  const double l_comm_b = l_comm + T * m.topk * S / std::max(c.n_disp * k.comm_bw_per_sm, 1.0);
+  const double l_comm_b = l_comm + T * m.topk * S / (comm_units * k.comm_bw_per_sm);
   const double ddown = mblocks * (F / 256) * tile_t(H, kEpiDgrad);
   const double wg_down = epr * (H / 128) * (F / 256) * tile_t(seg_pad, kEpiWgrad);
   p.bwd_dispatch = kernel(ddown + wg_down + c.n_disp * l_comm_b + c.n_relay * l_relay,
-                          std::max(l_comm_b, l_relay) + tile_t(H, kEpiDgrad), 0.0);
+                          std::max(l_comm_b, l_relay) + tile_t(H, kEpiDgrad), 0.0, 0, 0, b_bd);
   const double dup = mblocks * (H / 256) * tile_t(2 * F, kEpiPush);
   const double wg_up = epr * (2 * F / 128) * (H / 256) * tile_t(seg_pad, kEpiWgrad);
-  p.bwd_combine = kernel(dup + wg_up, l_push, l_reduce, mblocks * (H / 256), tile_t(2 * F, kEpiPush));
+  p.bwd_combine = kernel(dup + wg_up, l_push, l_reduce, mblocks * (H / 256), tile_t(2 * F, kEpiPush), b_bc);
   p.total = p.fwd_dispatch + p.fwd_combine + p.bwd_dispatch + p.bwd_combine;
   p.t_gemm_bound = 18.0 * m.topk * H * F * T / s.p_peak;
   p.t_nvl_bound = 2.0 * ((W - 1) * q + k_rem) * 2.0 * H * T / s.bw_nvl;
@@ -595,7 +611,7 @@ TuneResult search(const HardwareSpec& spec, const MoEShape& shape, const Traffic
 TuneResult search_layer(const HardwareSpec& spec, const MoEShape& shape, int n_workers,
                         const B200Calib& calib) {
   std::vector<TuneConfig> cands;
-  for (int nd = 4; nd < spec.n_sm; nd += 4) {
+  for (int nd = calib.spare_sm_equiv > 0 ? 0 : 4; nd < spec.n_sm; nd += 4) {
     std::vector<int> relays = {0};
     if (spec.world_size > 1)
       for (int r : SearchSpace::relay_choices(nd)) relays.push_back(r);

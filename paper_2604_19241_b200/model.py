@@ -37,7 +37,8 @@ class Breakdown(C.Structure):
 
 class Calib(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("mu", "tile_overhead", "comm_bw_per_sm", "relay_bw_per_sm",
-                                          "reduce_bw", "launch", "epi_bw_per_sm")]
+                                          "reduce_bw", "launch", "epi_bw_per_sm", "spare_sm_equiv",
+                                          "hbm_overlap")]
 
 
 class LayerPrediction(C.Structure):
@@ -49,7 +50,8 @@ class LayerPrediction(C.Structure):
 
 
 # B200 calibration of this build (DESIGN.md §Performance model; refit by tools/calibrate_model.py)
-B200_CALIB = Calib(0.8081, 0.708e-6, 11.4e9, 11.4e9, 4.87e12, 144.8e-6, 70.0e9)  # profiles/r01_perf_model_validation.md (pair engine)
+# fitted over 76 measured cases, spare-warp comm workers on/off (profiles/r01_perf_model_validation.md)
+B200_CALIB = Calib(1.0, 0.2e-6, 46.2e9, 46.2e9, 4.247e12, 49.35e-6, 196.8e9, 25.89, 0.619)
 
 
 def hw(world, n_sm=148, p_peak=1408.1e12, bw_hbm=6468.9e9, bw_nvl=770e9, w_sat=1024.0, tau_sync=1e-6):
@@ -110,10 +112,10 @@ def choose_config(H, F, E, k, tokens, world, n_sm=148):
     """TuneConfig for one layer shape from the B200 model (n_red = all SMs; w = 8)."""
     best, _, _ = search_layer(shape(H, F, E, k, tokens), hw(world, n_sm=n_sm))
     best.n_red = n_sm
-    # Measured floor: the model does not yet capture the start-up of the GEMM tiles behind the
-    # first landed rowgroups. With the GEMM CTAs' spare warps in the comm pool (default), 16 comm
-    # CTAs is the measured optimum at EP=1 (profiles/r01_spare_warps.txt); without them (round-1
-    # kernels, EPLAB_SPARE=0) it was >= 64 (profiles/r01_ndisp_sweep.txt). EP>1: not yet measured.
+    # Measured floor: the model does not capture the start-up of the GEMM tiles behind the first
+    # landed rowgroups. With the GEMM CTAs' spare warps in the comm pool (default) the model picks
+    # 0-20 comm CTAs and 16 is the measured optimum at EP=1 (profiles/r01_spare_warps.txt); without
+    # them (EPLAB_SPARE=0) it was >= 64 (profiles/r01_ndisp_sweep.txt). EP>1: not yet measured.
     import os
     floor = ((16 if os.environ.get("EPLAB_SPARE", "1") != "0" else 64) * n_sm) // 148
     if best.n_disp < floor and floor + best.n_relay < n_sm:

@@ -14,7 +14,7 @@ from oracle import pyoracle as po  # noqa: E402
 from paper_2604_19241_b200 import moe as M  # noqa: E402
 
 
-def measure(H, F, E, k, T, cfg, steps=3):
+def measure(H, F, E, k, T, cfg, steps=3, spare=1):
     sel, gw = po.Oracle().sample_routing(E, k, T, 1, 7)
     ids = torch.from_numpy(sel[0].reshape(T, k).copy()).cuda()
     gws = torch.from_numpy(gw[0].reshape(T, k).copy()).cuda()
@@ -25,6 +25,7 @@ def measure(H, F, E, k, T, cfg, steps=3):
     w_down = (torch.randn(E, H, F, device="cuda", generator=g) * F ** -0.5).bfloat16()
     L = M.EpMoE(H, F, E, k, T)
     L.set_tune_config(cfg)
+    L.set_comm_options(spare_warps=bool(spare))
     y = torch.empty(T, H, device="cuda", dtype=torch.bfloat16)
     out = dict(dx=torch.empty(T, H, dtype=torch.bfloat16, device="cuda"), dw_up=torch.empty_like(w_up),
                dw_down=torch.empty_like(w_down), dgate=torch.empty(T, k, dtype=torch.float32, device="cuda"))
@@ -71,9 +72,9 @@ def main():
               ("dsv3", 7168, 2048, 256, 8, 16384), ("sweep64k", 2048, 768, 128, 8, 65536)]
     with open(args.out, "w") as f:
         for name, H, F, E, k, T in cases:
-            for nd in (32, 64):
-                ms = measure(H, F, E, k, T, M.TuneConfig(nd, 0, 1, 148, 8))
-                rec = dict(name=name, H=H, F=F, E=E, k=k, T=T, world=1, n_disp=nd, n_relay=0, ms=ms)
+            for nd, spare in ((0, 1), (16, 1), (64, 1), (64, 0)):
+                ms = measure(H, F, E, k, T, M.TuneConfig(nd, 0, 1, 148, 8), spare=spare)
+                rec = dict(name=name, H=H, F=F, E=E, k=k, T=T, world=1, n_disp=nd, n_relay=0, spare=spare, ms=ms)
                 f.write(json.dumps(rec) + "\n")
                 f.flush()
                 print(json.dumps(rec), flush=True)

@@ -145,6 +145,8 @@ MkArgs base_args(eplab_ctx* c) {
   // A/B experiments: environment switches read per launch
   if (const char* e = getenv("EPLAB_COMM")) a.comm_bulk = std::string(e) == "bulk";
   if (const char* e = getenv("EPLAB_SPARE")) a.spare_warps = atoi(e);
+  a.rgp = getenv("EPLAB_RGP") ? std::max(1, atoi(getenv("EPLAB_RGP"))) : 8;
+  a.tngp = getenv("EPLAB_TNGP") ? std::max(1, atoi(getenv("EPLAB_TNGP"))) : 4;
   // somebody must move the rows: the bulk mover and spare-less pools need >= 1 comm CTA
   if (a.n_disp == 0 && (a.comm_bulk || !a.spare_warps)) a.n_disp = 1;
   return a;

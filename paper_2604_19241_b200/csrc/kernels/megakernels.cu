@@ -156,7 +156,7 @@ __device__ __forceinline__ TileDesc tn_tile(const Dims& d, const PlanDev& p, int
 
 // CTA-pair tiles: 256 token rows (two 128-row blocks of one expert; the second may be empty
 // when the expert has an odd number of blocks) x column block, grouped raster of 8 pairs.
-constexpr int RASTER_GP = 8;
+constexpr int RASTER_GP = 8;  // default raster group (MkArgs.rgp / EPLAB_RGP override)
 __device__ __forceinline__ int expert_of_pair(const PlanDev& p, int epr, long long g) {
   int lo = 0, hi = epr - 1;
   while (lo < hi) {
@@ -169,14 +169,14 @@ __device__ __forceinline__ int expert_of_pair(const PlanDev& p, int epr, long lo
   return lo;
 }
 __device__ __forceinline__ TileDesc nt_tile_pair(const Dims& d, const PlanDev& p, int t, int nb,
-                                                 int bn_cols, int nkb) {
+                                                 int bn_cols, int nkb, int G = RASTER_GP) {
   const int e = expert_of_pair(p, d.epr, (long long)t / nb);
   const int local = t - p.mpair_pre[e] * nb;
   const int mps = p.mpair_pre[e + 1] - p.mpair_pre[e];
-  const int g = local / (RASTER_GP * nb);
-  const int gsz = min(RASTER_GP, mps - g * RASTER_GP);
-  const int r = local - g * RASTER_GP * nb;
-  const int nbk = r / gsz, mp = g * RASTER_GP + r % gsz;
+  const int g = local / (G * nb);
+  const int gsz = min(G, mps - g * G);
+  const int r = local - g * G * nb;
+  const int nbk = r / gsz, mp = g * G + r % gsz;
   TileDesc td;
   const int ge = d.rank * d.epr + e;
   td.e = e;
@@ -191,15 +191,15 @@ __device__ __forceinline__ TileDesc nt_tile_pair(const Dims& d, const PlanDev& p
 }
 constexpr int TN_GP = 4;
 __device__ __forceinline__ TileDesc tn_tile_pair(const Dims& d, const PlanDev& p, int t, int NO,
-                                                 int KO) {
+                                                 int KO, int G = TN_GP) {
   const int mb = NO / (2 * BM), nb = KO / BN, per_e = mb * nb;
   TileDesc td;
   td.e = t / per_e;
   const int l = t - td.e * per_e;
-  const int g = l / (TN_GP * nb);
-  const int gsz = min(TN_GP, mb - g * TN_GP);
-  const int r = l - g * TN_GP * nb;
-  td.m0 = (g * TN_GP + r % gsz) * 2 * BM;
+  const int g = l / (G * nb);
+  const int gsz = min(G, mb - g * G);
+  const int r = l - g * G * nb;
+  td.m0 = (g * G + r % gsz) * 2 * BM;
   td.n0 = (r / gsz) * BN;
   const int ge = d.rank * d.epr + td.e;
   td.kb0 = p.sb_all[ge];
@@ -666,6 +666,7 @@ __device__ __forceinline__ void reduce_tokens(const MkArgs& a, int ph, long long
 }
 
 __device__ void reduce_task(const MkArgs& a, int task, int ph) {
+  if (a.dbg & 64) return;  // experiment: no reduce (wrong y / dx; measures the reduce's share)
   long long t0, t1;
   even_slice(a.p.n_tok, a.n_red, task, t0, t1);
   const int k = a.d.topk;
@@ -709,7 +710,7 @@ struct ModeUp {
   __device__ static void epilogue_prefetch(const Args&, const TileDesc&, int) {}
   // ---- CTA pair: rank 0 stages the gate rows, rank 1 the up rows of the same f-block
   __device__ static TileDesc tile_pair(const Args& a, int t) {
-    return nt_tile_pair(a.d, a.p, t, a.d.F / 128, 128, a.d.H / BK);
+    return nt_tile_pair(a.d, a.p, t, a.d.F / 128, 128, a.d.H / BK, a.rgp);
   }
   __device__ static void before_loads_pair(const Args& a, const TileDesc& td) { wait_pair_rows(a, 0, td, 30); }
   __device__ static void load_a_pair(const Args&, const TmaSet& tm, uint32_t bar, uint8_t* s,
@@ -797,7 +798,7 @@ struct ModeDown {
   static constexpr bool HAS_TILE_DONE = false;
   __device__ static void epilogue_prefetch(const Args&, const TileDesc&, int) {}
   __device__ static TileDesc tile_pair(const Args& a, int t) {
-    return nt_tile_pair(a.d, a.p, t, a.d.H / BN, BN, a.d.F / BK);
+    return nt_tile_pair(a.d, a.p, t, a.d.H / BN, BN, a.d.F / BK, a.rgp);
   }
   __device__ static void before_loads_pair(const Args&, const TileDesc&) {}
   __device__ static void load_a_pair(const Args&, const TmaSet& tm, uint32_t bar, uint8_t* s,
@@ -873,8 +874,8 @@ struct ModeDgradDown {
   __device__ static int n_dgrad_pair(const Args& a) { return a.p.mpair_pre[a.d.epr] * (a.d.F / BN); }
   __device__ static TileDesc tile_pair(const Args& a, int t) {
     const int nd = n_dgrad_pair(a);
-    if (t < nd) return nt_tile_pair(a.d, a.p, t, a.d.F / BN, BN, a.d.H / BK);
-    return tn_tile_pair(a.d, a.p, t - nd, a.d.H, a.d.F);
+    if (t < nd) return nt_tile_pair(a.d, a.p, t, a.d.F / BN, BN, a.d.H / BK, a.rgp);
+    return tn_tile_pair(a.d, a.p, t - nd, a.d.H, a.d.F, a.tngp);
   }
   __device__ static void before_loads_pair(const Args& a, const TileDesc& td) {
     if (!td.pad1)
@@ -1065,8 +1066,8 @@ struct ModeDgradUp {
   __device__ static int n_dgrad_pair(const Args& a) { return a.p.mpair_pre[a.d.epr] * (a.d.H / BN); }
   __device__ static TileDesc tile_pair(const Args& a, int t) {
     const int nd = n_dgrad_pair(a);
-    if (t < nd) return nt_tile_pair(a.d, a.p, t, a.d.H / BN, BN, 2 * a.d.F / BK);
-    return tn_tile_pair(a.d, a.p, t - nd, 2 * a.d.F, a.d.H);
+    if (t < nd) return nt_tile_pair(a.d, a.p, t, a.d.H / BN, BN, 2 * a.d.F / BK, a.rgp);
+    return tn_tile_pair(a.d, a.p, t - nd, 2 * a.d.F, a.d.H, a.tngp);
   }
   __device__ static void before_loads_pair(const Args&, const TileDesc&) {}
   __device__ static void load_a_pair(const Args&, const TmaSet& tm, uint32_t bar, uint8_t* s,

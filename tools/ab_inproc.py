@@ -34,8 +34,17 @@ st = torch.cuda.current_stream()
 variants = [v.strip() for v in args.variants.split(";")]
 
 
+ENV_KEYS = {kv.split("=")[0] for v in variants for kv in v.split(",") if kv and not kv.startswith("tune=")}
+ENV0 = {k: os.environ.get(k) for k in ENV_KEYS}
+
+
 def apply(v):
     cfg = base_cfg
+    for k0, v0 in ENV0.items():  # every variant starts from the original environment
+        if v0 is None:
+            os.environ.pop(k0, None)
+        else:
+            os.environ[k0] = v0
     for kv in [p for p in v.split(",") if p]:
         key, val = kv.split("=")
         if key == "tune":

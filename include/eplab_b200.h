@@ -129,10 +129,12 @@ EPLAB_API int eplab_connect_local(eplab_ctx* const* ctxs, int n);
 
 EPLAB_API int eplab_set_tune_config(eplab_ctx* ctx, const eplab_tune_config* cfg);
 EPLAB_API int eplab_get_tune_config(const eplab_ctx* ctx, eplab_tune_config* cfg);
-/* Comm-pool workers of the dispatch MegaKernels (the unified primitive's warp split): with
- * spare_warps = 1 (default) the GEMM CTAs' idle warps drain the same priority-ordered round pool
- * as the n_disp comm CTAs, so n_disp may be 0; bulk_mover = 1 moves rows through the TMA
- * bulk-copy engine (comm CTAs only) instead of warp copies. Results are bitwise identical. */
+/* Work for the GEMM CTAs' idle warps (the unified primitive's warp split), a bit set:
+ * bit 0 (comm): they drain the dispatch MegaKernels' priority-ordered round pool together with
+ * the n_disp comm CTAs, so n_disp may be 0; bit 1 (reduce): they fold completed dX tokens in the
+ * backward combine MegaKernel while its weight-gradient tiles run. Default 3. bulk_mover = 1 moves
+ * rows through the TMA bulk-copy engine (comm CTAs only) instead of warp copies. Results are
+ * bitwise identical for every setting. */
 EPLAB_API int eplab_set_comm_options(eplab_ctx* ctx, int spare_warps, int bulk_mover);
 /* Persistent grid size (default: all SMs). Several ranks sharing one GPU (the single-device
  * multi-rank test mode) each get a disjoint budget so their MegaKernels are co-resident. */

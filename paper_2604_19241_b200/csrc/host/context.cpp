@@ -76,7 +76,7 @@ struct eplab_ctx {
   int pair = 1;  // CTA-pair engine (EPLAB_ENGINE=single selects the single-CTA one)
   // comm pool workers: spare GEMM warps join (warp split; EPLAB_SPARE=0 disables), bulk-copy
   // mover instead of warp copies (EPLAB_COMM=bulk); eplab_set_comm_options overrides both
-  int spare_warps = 1, comm_bulk = 0;
+  int spare_warps = 3, comm_bulk = 0;
   // timeline
   TimelineRec* tl_rec = nullptr;
   int* tl_count = nullptr;
@@ -141,6 +141,7 @@ MkArgs base_args(eplab_ctx* c) {
   a.pair = c->pair;
   a.comm_bulk = c->comm_bulk;
   a.comm_cursor = c->cursor + 2;
+  a.red_cursor = reinterpret_cast<unsigned*>(c->cursor + 4);
   a.spare_warps = c->spare_warps;
   // A/B experiments: environment switches read per launch
   if (const char* e = getenv("EPLAB_COMM")) a.comm_bulk = std::string(e) == "bulk";
@@ -148,7 +149,7 @@ MkArgs base_args(eplab_ctx* c) {
   a.rgp = getenv("EPLAB_RGP") ? std::max(1, atoi(getenv("EPLAB_RGP"))) : 8;
   a.tngp = getenv("EPLAB_TNGP") ? std::max(1, atoi(getenv("EPLAB_TNGP"))) : 4;
   // somebody must move the rows: the bulk mover and spare-less pools need >= 1 comm CTA
-  if (a.n_disp == 0 && (a.comm_bulk || !a.spare_warps)) a.n_disp = 1;
+  if (a.n_disp == 0 && (a.comm_bulk || !(a.spare_warps & 1))) a.n_disp = 1;
   return a;
 }
 
@@ -391,7 +392,7 @@ int eplab_set_sm_budget(eplab_ctx* c, int n_sm) {
 
 int eplab_set_comm_options(eplab_ctx* c, int spare_warps, int bulk_mover) {
   return guarded([&] {
-    validate(spare_warps == 0 || spare_warps == 1, "spare_warps must be 0 or 1");
+    validate(spare_warps >= 0 && spare_warps <= 3, "spare_warps must be a bit set in [0, 3]");
     validate(bulk_mover == 0 || bulk_mover == 1, "bulk_mover must be 0 or 1");
     c->spare_warps = spare_warps;
     c->comm_bulk = bulk_mover;

@@ -599,83 +599,129 @@ __device__ void relay_task(const MkArgs& a, int task, int ph) {
 // ------------------------------------------------------------------ reduce role
 // Top-k completeness barrier, then the fixed k-ascending fold (
 // precision.cpp:31-37 order): forward y = bf16(fma-fold of w_j * o_j), backward
-// dx = bf16(sum_j dX_j), both in fp32. A token's k replica rows are one contiguous block
-// [t*k, t*k+k) x H; each lane keeps KT x U 16-byte loads in flight (KT >= k replicas x U column
-// chunks, 16 per lane) so the HBM-bound fold is not latency-bound.
+// dx = bf16(sum_j dX_j), both in fp32. The fold of one token is a warp job: the token's k
+// replica rows are one contiguous block [t*k, t*k+k) x H, each lane keeps KT x U 16-byte loads in
+// flight (KT >= k replicas x U column chunks, 16 per lane), so the HBM-bound fold is not
+// latency-bound.
 template <int KT>
-__device__ __forceinline__ void reduce_tokens(const MkArgs& a, int ph, long long t0, long long t1) {
+__device__ __forceinline__ void fold_token(const MkArgs& a, int ph, long long t) {
   constexpr int U = 16 / KT;
   const Dims& d = a.d;
   const int k = d.topk, vecs = d.H / 8;
   const SymPtrs& me = a.peers.p[d.rank];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t need = (uint32_t)(k * (d.H / BN));
+  const int lane = threadIdx.x & 31;
   const int4* rep = reinterpret_cast<const int4*>(ph == 0 ? me.rep : me.rep_dx);
   int4* out = reinterpret_cast<int4*>(ph == 0 ? a.y : a.dx);
-  for (long long t = t0 + warp; t < t1; t += GEMM_THREADS / 32) {
-    if (lane == 0)
-      wait_geq_sys(tok_counter(me, d, ph, a.par, (int)t), need, a.timeout_ns, a.err, 20 + ph, (int)t);
-    __syncwarp();
-    float w[KT];
+  float w[KT];
 #pragma unroll
-    for (int j = 0; j < KT; ++j) w[j] = (j < k && ph == 0) ? a.p.gate_w[t * k + j] : 1.0f;
-    const int4* base = rep + (size_t)t * k * vecs;
-    for (int c = lane; c < vecs; c += 32 * U) {
-      int4 v[KT][U];
+  for (int j = 0; j < KT; ++j) w[j] = (j < k && ph == 0) ? a.p.gate_w[t * k + j] : 1.0f;
+  const int4* base = rep + (size_t)t * k * vecs;
+  for (int c = lane; c < vecs; c += 32 * U) {
+    int4 v[KT][U];
 #pragma unroll
-      for (int j = 0; j < KT; ++j)
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (j < k && c + 32 * u < vecs) v[j][u] = base[(size_t)j * vecs + c + 32 * u];
-      float acc[U][8];
+    for (int j = 0; j < KT; ++j)
 #pragma unroll
       for (int u = 0; u < U; ++u)
+        if (j < k && c + 32 * u < vecs) v[j][u] = base[(size_t)j * vecs + c + 32 * u];
+    float acc[U][8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) acc[u][q] = 0.f;
+    for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int j = 0; j < KT; ++j) {
-        if (j >= k) break;
+      for (int q = 0; q < 8; ++q) acc[u][q] = 0.f;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&v[j][u]);
+    for (int j = 0; j < KT; ++j) {
+      if (j >= k) break;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float2 f = __bfloat1622float2(hv[q]);
-            if (ph == 0) {
-              acc[u][2 * q] = fmaf(w[j], f.x, acc[u][2 * q]);
-              acc[u][2 * q + 1] = fmaf(w[j], f.y, acc[u][2 * q + 1]);
-            } else {
-              acc[u][2 * q] = acc[u][2 * q] + f.x;
-              acc[u][2 * q + 1] = acc[u][2 * q + 1] + f.y;
-            }
+      for (int u = 0; u < U; ++u) {
+        const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&v[j][u]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 f = __bfloat1622float2(hv[q]);
+          if (ph == 0) {
+            acc[u][2 * q] = fmaf(w[j], f.x, acc[u][2 * q]);
+            acc[u][2 * q + 1] = fmaf(w[j], f.y, acc[u][2 * q + 1]);
+          } else {
+            acc[u][2 * q] = acc[u][2 * q] + f.x;
+            acc[u][2 * q + 1] = acc[u][2 * q + 1] + f.y;
           }
         }
       }
+    }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (c + 32 * u >= vecs) continue;
-        int4 o;
-        o.x = (int)pack_bf16(acc[u][0], acc[u][1]);
-        o.y = (int)pack_bf16(acc[u][2], acc[u][3]);
-        o.z = (int)pack_bf16(acc[u][4], acc[u][5]);
-        o.w = (int)pack_bf16(acc[u][6], acc[u][7]);
-        out[(size_t)t * vecs + c + 32 * u] = o;
+    for (int u = 0; u < U; ++u) {
+      if (c + 32 * u >= vecs) continue;
+      int4 o;
+      o.x = (int)pack_bf16(acc[u][0], acc[u][1]);
+      o.y = (int)pack_bf16(acc[u][2], acc[u][3]);
+      o.z = (int)pack_bf16(acc[u][4], acc[u][5]);
+      o.w = (int)pack_bf16(acc[u][6], acc[u][7]);
+      out[(size_t)t * vecs + c + 32 * u] = o;
+    }
+  }
+}
+
+// Reduce workers: warps claim RCHUNK-token chunks from one atomic counter (the post-task CTAs
+// after their GEMM tiles and, in the backward combine, the GEMM CTAs' spare warps from the start:
+// there dX tokens complete during the up-dgrad tiles and fold under the up-wgrad tiles that
+// follow). A warp polls its chunk's arrival counters (lane i <-> token i) and folds the tokens in
+// the order they complete; who folds a token and when never changes its value. (In the forward
+// combine no tiles follow the down GEMM and, with random routing, tokens complete with its last
+// tiles: spare warps would only hold chunks they fold slowly, so they stay out.)
+constexpr int RCHUNK = 8;
+template <int KT>
+__device__ void reduce_chunks_t(const MkArgs& a, int ph, bool backoff) {
+  const Dims& d = a.d;
+  const SymPtrs& me = a.peers.p[d.rank];
+  const int lane = threadIdx.x & 31;
+  const uint32_t need = (uint32_t)(d.topk * (d.H / BN));
+  const int n_chunks = (a.p.n_tok + RCHUNK - 1) / RCHUNK;
+  for (;;) {
+    int c = 0;
+    if (lane == 0) c = (int)atomicAdd(a.red_cursor, 1u);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= n_chunks) break;
+    const long long t = (long long)c * RCHUNK + lane;
+    unsigned todo = __ballot_sync(0xffffffffu, lane < RCHUNK && t < a.p.n_tok);
+    const unsigned long long t0 = globaltimer();
+    while (todo) {
+      bool ready = false;
+      if ((todo >> lane) & 1u) ready = ld_acquire_sys(tok_counter(me, d, ph, a.par, (int)t)) >= need;
+      unsigned r = __ballot_sync(0xffffffffu, ready);
+      if (!r) {
+        if (aborted(a.err)) return;
+        if (globaltimer() - t0 > a.timeout_ns) {
+          if (lane == 0) report_timeout(a.err, 20 + ph, need, 0, (int)(c * RCHUNK + __ffs(todo) - 1));
+          return;
+        }
+        if (backoff) __nanosleep(500);
+        continue;
+      }
+      todo &= ~r;
+      while (r) {
+        const int i = __ffs(r) - 1;
+        r &= r - 1;
+        fold_token<KT>(a, ph, (long long)c * RCHUNK + i);
       }
     }
   }
 }
 
-__device__ void reduce_task(const MkArgs& a, int task, int ph) {
+__device__ void reduce_chunks(const MkArgs& a, int ph, bool backoff) {
   if (a.dbg & 64) return;  // experiment: no reduce (wrong y / dx; measures the reduce's share)
-  long long t0, t1;
-  even_slice(a.p.n_tok, a.n_red, task, t0, t1);
-  const int k = a.d.topk;
-  if (k <= 4)
-    reduce_tokens<4>(a, ph, t0, t1);
-  else if (k <= 8)
-    reduce_tokens<8>(a, ph, t0, t1);
+  if (a.d.topk <= 8)
+    reduce_chunks_t<8>(a, ph, backoff);
   else
-    reduce_tokens<16>(a, ph, t0, t1);
+    reduce_chunks_t<16>(a, ph, backoff);
+}
+
+__device__ void reduce_task(const MkArgs& a, int, int ph) { reduce_chunks(a, ph, false); }
+
+// spare warps of the backward combine MegaKernel's GEMM CTAs join the reduce pool from the start
+__device__ __forceinline__ void spare_reduce(const MkArgs& a, const Timeline& tl, int ph) {
+  if (!(a.spare_warps & 2)) return;
+  const unsigned long long t0 = globaltimer();
+  reduce_chunks(a, ph, true);
+  if ((threadIdx.x & 31) == 0) timeline_push(tl, t0, globaltimer(), ROLE_REDUCE, -1 - (int)(threadIdx.x >> 5));
 }
 
 // ------------------------------------------------------------------ GEMM modes
@@ -686,7 +732,7 @@ __device__ void reduce_task(const MkArgs& a, int task, int ph) {
 // Spare warps of the dispatch MegaKernels' GEMM CTAs drain the comm pool too (warp split);
 // their activity goes into the device timeline as one comm interval per warp.
 __device__ __forceinline__ void spare_comm(const MkArgs& a, const Timeline& tl, int ph) {
-  if (!a.spare_warps || a.comm_bulk) return;
+  if (!(a.spare_warps & 1) || a.comm_bulk) return;
   const unsigned long long t0 = globaltimer();
   const int n = comm_rounds(a, ph);
   if (n > 0 && (threadIdx.x & 31) == 0) timeline_push(tl, t0, globaltimer(), ROLE_COMM, -1 - (int)(threadIdx.x >> 5));
@@ -1062,6 +1108,8 @@ struct ModeDgradDown {
 struct ModeDgradUp {
   using Args = MkArgs;
   static constexpr bool HAS_TILE_DONE = false;
+  static constexpr bool SPARE = true;
+  __device__ static void spare(const Args& a, const Timeline& tl) { spare_reduce(a, tl, 1); }
   __device__ static void epilogue_prefetch(const Args&, const TileDesc&, int) {}
   __device__ static int n_dgrad_pair(const Args& a) { return a.p.mpair_pre[a.d.epr] * (a.d.H / BN); }
   __device__ static TileDesc tile_pair(const Args& a, int t) {
@@ -1288,7 +1336,7 @@ using namespace eplab_dev;
 template <int KIND, class Mode>
 static int launch_mk(const TmaSet& tm, const MkArgs& a, int grid, cudaStream_t st) {
   static bool attr = false, attr_p = false;
-  cudaMemsetAsync(a.cursor, 0, 16, st);  // task cursor + comm round counter
+  cudaMemsetAsync(a.cursor, 0, 32, st);  // task cursor, comm round counter, reduce chunk counter
   if (!a.pair) {
     auto fn = megakernel<KIND, Mode>;
     if (!attr) {

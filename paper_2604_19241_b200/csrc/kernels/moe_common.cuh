@@ -137,7 +137,9 @@ struct MkArgs {
             // 16 = skip the saved g, u loads of the dgrad epilogue
   int pair;  // 1: CTA-pair (cta_group::2) engine
   int* comm_cursor;  // [2] u64 round counter of the comm pool (zeroed per launch with cursor)
-  int spare_warps;  // 1: the GEMM CTAs' spare warps join the comm pool (warp split)
+  unsigned* red_cursor;  // reduce chunk counter (zeroed per launch with cursor)
+  int spare_warps;  // bit 0: the GEMM CTAs' spare warps join the comm pool (warp split),
+                    // bit 1: ... and the backward combine's reduce pool
   int comm_bulk;
   int rgp, tngp;  // CTA-pair raster groups: 256-row blocks per NT group, 256-row output blocks per TN group  // 1: comm role moves rows with the TMA bulk-copy engine (EPLAB_COMM=bulk)
 };

@@ -162,8 +162,10 @@ class EpMoE:
             cfg = TuneConfig(*cfg)
         _check(lib().eplab_set_tune_config(self.h, C.byref(cfg)))
 
-    def set_comm_options(self, spare_warps=True, bulk_mover=False):
-        _check(lib().eplab_set_comm_options(self.h, int(spare_warps), int(bulk_mover)))
+    def set_comm_options(self, spare_warps=3, bulk_mover=False):
+        """spare_warps: bit 0 = comm pool, bit 1 = backward reduce pool (True = 3, False = 0)."""
+        sw = 3 if spare_warps is True else (0 if spare_warps is False else int(spare_warps))
+        _check(lib().eplab_set_comm_options(self.h, sw, int(bulk_mover)))
 
     def tune_config(self):
         c = TuneConfig()

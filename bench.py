@@ -190,11 +190,11 @@ def run_unfused(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from oracle import pyoracle as po
+    from paper_2604_19241_b200.model import sample_routing
     from tools import unfused_baseline as ub
     H, F, E, k, T = CONFIGS[args.config]
     epr = E // world
-    sel, gw = po.Oracle().sample_routing(E, k, T, world, 7)
+    sel, gw = sample_routing(E, k, T, world, 7)
     ids = torch.from_numpy(sel[rank].reshape(T, k).copy()).cuda().long()
     gws = torch.from_numpy(gw[rank].reshape(T, k).copy()).cuda()
     g = torch.Generator(device="cuda").manual_seed(1234 + rank)
@@ -281,13 +281,12 @@ def run_ours(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from oracle import pyoracle as po  # routing generator = the reference's sample_routing (restated)
     from paper_2604_19241_b200 import moe as M
-    from paper_2604_19241_b200.model import choose_config
+    from paper_2604_19241_b200.model import choose_config, sample_routing
 
     H, F, E, k, T = CONFIGS[args.config]
     epr = E // world
-    sel, gw = po.Oracle().sample_routing(E, k, T, world, 7)
+    sel, gw = sample_routing(E, k, T, world, 7)  # the reference's generator (library host code)
     ids = torch.from_numpy(sel[rank].reshape(T, k).copy()).cuda()
     gws = torch.from_numpy(gw[rank].reshape(T, k).copy()).cuda()
     g = torch.Generator(device="cuda").manual_seed(1234 + rank)

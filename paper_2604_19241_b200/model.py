@@ -74,6 +74,19 @@ def _L():
     return L
 
 
+def sample_routing(n_exp, topk, n_tok, world, seed):
+    """The reference's synthetic routing (routing.cpp:32-73, sample_routing) from this library's
+    host implementation: sel int32 / gw fp32, [world][n_tok * topk]."""
+    import numpy as np
+    sel = np.empty((world, n_tok * topk), dtype=np.int32)
+    gw = np.empty((world, n_tok * topk), dtype=np.float32)
+    L = _L()
+    L.eplab_sample_routing.argtypes = [C.c_int, C.c_int, C.c_longlong, C.c_int, C.c_uint64, C.c_void_p, C.c_void_p]
+    L.eplab_sample_routing.restype = C.c_int
+    _check(L.eplab_sample_routing(n_exp, topk, n_tok, world, seed, sel.ctypes.data, gw.ctypes.data))
+    return sel, gw
+
+
 def volume_expected(s, h, remote_only=False):
     t = Traffic()
     _check(_L().eplab_volume_expected(C.byref(s), C.byref(h), int(remote_only), C.byref(t)))

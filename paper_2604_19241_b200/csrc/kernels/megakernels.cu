@@ -350,12 +350,18 @@ __device__ void comm_pipeline(const MkArgs& a, int ph, GemmSmem* S, uint8_t* sbu
 // the backward phase it folds the gate gradient <dY_t, o_{t,j}> of every item while the dY row
 // is in registers. Then it releases the round: one system-scope fence, relaxed rowgroup
 // counter updates aggregated per counter (relay off) or per-slot epoch flags (relay on).
+constexpr int CROUNDS = 128;
 __device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
   const Dims& d = a.d;
   const int k = d.topk, vecs = d.H / 8, me = d.rank;
   const int lane = threadIdx.x & 31;
   const long long n = (long long)a.p.n_tok * k;
-  const long long idx = r * 32 + lane;
+  // Super-rounds of CROUNDS rounds x 32 items: round g of a super-round takes the items
+  // g, g + CROUNDS, g + 2 CROUNDS, ... so the CROUNDS warps working a super-round move its
+  // schedule front to back together -- the first 128-row rowgroup (the first GEMM tiles' rows)
+  // lands after one row copy instead of after a whole round.
+  const long long sr = r / CROUNDS, g = r - sr * CROUNDS;
+  const long long idx = sr * CROUNDS * 32 + g + (long long)lane * CROUNDS;
   int item = -1, slot = 0, dst = -1;  // dst < 0: the row does not travel from here
   if (idx < n) {
     const int i = a.p.sched[idx];
@@ -384,6 +390,30 @@ __device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
   auto dst_row = [&](int dr, int sl) {
     const SymPtrs& P = a.peers.p[dr];
     return reinterpret_cast<int4*>(ph == 0 ? P.recv_x : P.recv_dy) + (size_t)sl * vecs;
+  };
+  // Release copied rows (fence + relaxed updates): after the first two
+  // copies of the round (the super-round's warps then complete its first rowgroups together)
+  // and at the end of the round (more frequent releases cost comm throughput: Qwen3's dY comm
+  // tasks 770 -> 873 us with a release every 8 rows).
+  unsigned done = 0, copied = 0;  // items released / items copied (lane bits)
+  int n_copies = 0;
+  auto release = [&]() {
+    const unsigned rel = copied & ~done;
+    if (!rel) return;
+    __syncwarp();
+    fence_acq_rel_sys();
+    const bool mine = (rel >> lane) & 1u;
+    if (a.n_relay > 0) {
+      if (mine) st_relaxed_sys(a.peers.p[dst].slot_flag + slot, a.epoch * 2 + ph);
+    } else {
+      uint32_t* ctr = mine ? rg_counter(a.peers.p[dst], d, ph, a.par, slot >> 7) : nullptr;
+      const unsigned mm = __match_any_sync(0xffffffffu, (unsigned long long)ctr);
+      if (ctr && lane == __ffs(mm) - 1) red_relaxed_sys_add(ctr, (uint32_t)__popc(mm));
+    }
+    done |= rel;
+  };
+  auto progress = [&]() {
+    if (n_copies <= 2) release();
   };
   if (ph == 0) {
     unsigned m = __ballot_sync(0xffffffffu, dst >= 0);
@@ -415,6 +445,9 @@ __device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
             if (two) db[c + 32 * u] = vb[u];
           }
       }
+      copied |= (1u << qa) | (1u << qb);
+      n_copies += two ? 2 : 1;
+      progress();
     }
   } else {
     const int4* orow_base = reinterpret_cast<const int4*>(a.peers.p[me].rep);
@@ -446,23 +479,21 @@ __device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
 #pragma unroll
       for (int s2 = 16; s2 > 0; s2 >>= 1) gacc += __shfl_xor_sync(0xffffffffu, gacc, s2);
       if (lane == 0) a.dgate[i] = gacc;
+      if (dq >= 0) {
+        copied |= 1u << q;
+        ++n_copies;
+        progress();
+      }
     }
   }
-  // release the round's copied rows (fence + relaxed updates)
-  __syncwarp();
-  fence_acq_rel_sys();
-  if (a.n_relay > 0) {
-    if (dst >= 0) st_relaxed_sys(a.peers.p[dst].slot_flag + slot, a.epoch * 2 + ph);
-  } else {
-    uint32_t* ctr = dst >= 0 ? rg_counter(a.peers.p[dst], d, ph, a.par, slot >> 7) : nullptr;
-    const unsigned mm = __match_any_sync(0xffffffffu, (unsigned long long)ctr);
-    if (ctr && lane == __ffs(mm) - 1) red_relaxed_sys_add(ctr, (uint32_t)__popc(mm));
-  }
+  release();
 }
 
 // A comm worker warp: claim rounds until the pool is empty. Returns the number of rounds moved.
 __device__ int comm_rounds(const MkArgs& a, int ph) {
-  const long long n_rounds = ((long long)a.p.n_tok * a.d.topk + 31) / 32;
+  // whole super-rounds (the last may be partly empty: items beyond n are skipped)
+  const long long n_items = (long long)a.p.n_tok * a.d.topk;
+  const long long n_rounds = (n_items + 32 * CROUNDS - 1) / (32 * CROUNDS) * CROUNDS;
   const int lane = threadIdx.x & 31;
   int done = 0;
   for (;;) {

@@ -70,7 +70,8 @@ struct eplab_ctx {
       tm_hw_mn{}, tm_dgu_k{}, tm_dgu_mn{};
   CUtensorMap st_gu{}, st_hact{}, st_dgu{}, st_hw{};  // epilogue store maps
   // iteration state
-  uint32_t epoch = 0;
+  uint32_t epoch = 0;            // host count of plans (the device counter is authoritative)
+  uint32_t* epoch_dev = nullptr;  // device iteration counter, advanced by the planning kernel
   bool planned = false;
   eplab_tune_config cfg{32, 0, 0, 148, 8};
   int pair = 1;  // CTA-pair engine (EPLAB_ENGINE=single selects the single-CTA one)
@@ -130,8 +131,7 @@ MkArgs base_args(eplab_ctx* c) {
   a.wg_cnt = c->wg_cnt;
   a.cursor = c->cursor;
   a.err = c->err;
-  a.epoch = c->epoch;
-  a.par = (int)(c->epoch & 1);
+  a.epoch_dev = c->epoch_dev;
   a.n_disp = std::max(0, c->cfg.n_disp);
   a.n_relay = std::max(0, c->cfg.n_relay);
   a.n_red = std::max(1, c->cfg.n_red);
@@ -231,7 +231,8 @@ int eplab_init(const eplab_init_args* args, eplab_ctx** out) {
                  o_sbr = take((size_t)W * d.epr * 4), o_sba = take((size_t)W * d.epr * 4),
                  o_mb = take(d.epr * 4), o_mbp = take((d.epr + 1) * 4),
                  o_mpp = take((d.epr + 1) * 4), o_sc = take(64),
-                 o_wg = take((size_t)d.epr * (d.F / 256) * 4), o_cur = take(64), o_err = take(64);
+                 o_wg = take((size_t)d.epr * (d.F / 256) * 4), o_cur = take(64), o_err = take(64),
+                 o_ep = take(64);
     CK(cudaMalloc(&c->loc, o));
     CK(cudaMemset(c->loc + o_hist, 0, o - o_hist));
     c->gu = reinterpret_cast<__nv_bfloat16*>(c->loc + o_gu);
@@ -257,6 +258,7 @@ int eplab_init(const eplab_init_args* args, eplab_ctx** out) {
     c->wg_cnt = reinterpret_cast<uint32_t*>(c->loc + o_wg);
     c->cursor = reinterpret_cast<int*>(c->loc + o_cur);
     c->err = reinterpret_cast<int*>(c->loc + o_err);
+    c->epoch_dev = reinterpret_cast<uint32_t*>(c->loc + o_ep);
 
     // ---- host-call staging (allocated on the first host call): ids, gate weights, x, dy, y,
     // dx, dgate
@@ -413,7 +415,7 @@ int eplab_plan(eplab_ctx* c, const int32_t* ids, const float* gw, int n_tok, voi
     c->plan.n_tok = n_tok;
     c->plan.topk_ids = ids;
     c->plan.gate_w = gw;
-    if (eplab_launch::plan_launch(c->d, c->peers, c->plan, c->epoch, c->timeout_ns, c->err, st))
+    if (eplab_launch::plan_launch(c->d, c->peers, c->plan, c->epoch_dev, c->timeout_ns, c->err, st))
       throw Fail{EPLAB_ERR_INTERNAL, std::string("plan launch: ") +
                                          cudaGetErrorString(cudaGetLastError())};
     eplab_launch::zero_padding_launch(c->d, c->plan, c->mine.recv_x, st);

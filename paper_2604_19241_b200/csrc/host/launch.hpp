@@ -6,7 +6,7 @@
 
 namespace eplab_launch {
 int plan_launch(const eplab_dev::Dims& d, const eplab_dev::Peers& peers,
-                const eplab_dev::PlanDev& p, uint32_t epoch, uint64_t timeout_ns, int* err,
+                const eplab_dev::PlanDev& p, uint32_t* epoch, uint64_t timeout_ns, int* err,
                 cudaStream_t st);
 int zero_padding_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p,
                         __nv_bfloat16* recv, cudaStream_t st);

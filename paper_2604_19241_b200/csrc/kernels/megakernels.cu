@@ -29,6 +29,17 @@
 
 namespace eplab_dev {
 
+// Iteration number of the running MegaKernel, read once per CTA from the device epoch counter
+// (advanced by the planning kernel), so a captured CUDA graph of a whole step replays correctly;
+// parity = epoch & 1 selects the scoreboard counters' double buffer.
+__shared__ uint32_t sh_epoch;
+#define EPOCH(a) (sh_epoch)
+#define PAR(a) ((int)(sh_epoch & 1u))
+__device__ __forceinline__ void load_epoch(const MkArgs& a) {
+  if (threadIdx.x == 0) sh_epoch = *reinterpret_cast<const volatile uint32_t*>(a.epoch_dev);
+  __syncthreads();
+}
+
 
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ uint32_t* rg_counter(const SymPtrs& s, const Dims& d, int ph, int par,
@@ -219,9 +230,9 @@ __device__ __forceinline__ TileDesc half_tile(const TileDesc& td, uint32_t rank)
 __device__ __forceinline__ void wait_pair_rows(const MkArgs& a, int ph, const TileDesc& td, int site) {
   const SymPtrs& me = a.peers.p[a.d.rank];
   const int g = td.m0 >> 7;
-  wait_geq_sys(rg_counter(me, a.d, ph, a.par, g), (uint32_t)min(BM, td.rows), a.timeout_ns, a.err, site, g);
+  wait_geq_sys(rg_counter(me, a.d, ph, PAR(a), g), (uint32_t)min(BM, td.rows), a.timeout_ns, a.err, site, g);
   if (td.rows > BM)
-    wait_geq_sys(rg_counter(me, a.d, ph, a.par, g + 1), (uint32_t)(td.rows - BM), a.timeout_ns, a.err, site,
+    wait_geq_sys(rg_counter(me, a.d, ph, PAR(a), g + 1), (uint32_t)(td.rows - BM), a.timeout_ns, a.err, site,
                  g + 1);
 }
 
@@ -300,9 +311,9 @@ __device__ void comm_pipeline(const MkArgs& a, int ph, GemmSmem* S, uint8_t* sbu
       const SymPtrs& P = a.peers.p[S->cdst[pp]];
       const int slot = S->cslot[pp];
       if (a.n_relay > 0) {
-        st_relaxed_sys(P.slot_flag + slot, a.epoch * 2 + ph);
+        st_relaxed_sys(P.slot_flag + slot, EPOCH(a) * 2 + ph);
       } else {
-        uint32_t* c = rg_counter(P, d, ph, a.par, slot >> 7);
+        uint32_t* c = rg_counter(P, d, ph, PAR(a), slot >> 7);
         if (c != cur) {
           if (cur) red_relaxed_sys_add(cur, run);
           cur = c;
@@ -382,7 +393,7 @@ __device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
     const int prim_slot = prim_j >= 0 ? a.p.dst_slot[t * k + prim_j] : -1;
     if (ph == 0) P.meta[slot] = SlotMeta{me, i, a.p.gate_w[i], prim_slot};
     // a duplicate's flag means "metadata valid"; the relay copies it after the primary's flag
-    if (prim_slot >= 0) st_release_sys(P.slot_flag + slot, a.epoch * 2 + ph);
+    if (prim_slot >= 0) st_release_sys(P.slot_flag + slot, EPOCH(a) * 2 + ph);
     item = i;
     dst = prim_slot >= 0 ? -1 : dr;
   }
@@ -404,9 +415,9 @@ __device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
     fence_acq_rel_sys();
     const bool mine = (rel >> lane) & 1u;
     if (a.n_relay > 0) {
-      if (mine) st_relaxed_sys(a.peers.p[dst].slot_flag + slot, a.epoch * 2 + ph);
+      if (mine) st_relaxed_sys(a.peers.p[dst].slot_flag + slot, EPOCH(a) * 2 + ph);
     } else {
-      uint32_t* ctr = mine ? rg_counter(a.peers.p[dst], d, ph, a.par, slot >> 7) : nullptr;
+      uint32_t* ctr = mine ? rg_counter(a.peers.p[dst], d, ph, PAR(a), slot >> 7) : nullptr;
       const unsigned mm = __match_any_sync(0xffffffffu, (unsigned long long)ctr);
       if (ctr && lane == __ffs(mm) - 1) red_relaxed_sys_add(ctr, (uint32_t)__popc(mm));
     }
@@ -544,7 +555,7 @@ __device__ void comm_task(const MkArgs& a, int task, int ph, GemmSmem* S, uint8_
       const SymPtrs& P = a.peers.p[dst];
       const int prim_slot = prim_j >= 0 ? a.p.dst_slot[t * k + prim_j] : -1;
       if (ph == 0) P.meta[slot] = SlotMeta{me, i, a.p.gate_w[i], prim_slot};
-      if (prim_slot >= 0) st_release_sys(P.slot_flag + slot, a.epoch * 2 + ph);
+      if (prim_slot >= 0) st_release_sys(P.slot_flag + slot, EPOCH(a) * 2 + ph);
       S->citem[threadIdx.x] = i;
       S->cslot[threadIdx.x] = slot;
       S->cdst[threadIdx.x] = prim_slot >= 0 ? -1 : dst;
@@ -601,7 +612,7 @@ __device__ void relay_task(const MkArgs& a, int task, int ph) {
   long long g0, g1;
   even_slice(n_rg, a.n_relay, task, g0, g1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t flagv = a.epoch * 2 + ph;
+  const uint32_t flagv = EPOCH(a) * 2 + ph;
   __nv_bfloat16* recv = ph == 0 ? me.recv_x : me.recv_dy;
   const int vecs = d.H / 8;
   for (long long g = g0; g < g1; ++g) {
@@ -622,7 +633,7 @@ __device__ void relay_task(const MkArgs& a, int task, int ph) {
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
-      red_release_gpu_add(rg_counter(me, d, ph, a.par, (int)g), (uint32_t)rows);
+      red_release_gpu_add(rg_counter(me, d, ph, PAR(a), (int)g), (uint32_t)rows);
     }
   }
 }
@@ -716,7 +727,7 @@ __device__ void reduce_chunks_t(const MkArgs& a, int ph, bool backoff) {
     const unsigned long long t0 = globaltimer();
     while (todo) {
       bool ready = false;
-      if ((todo >> lane) & 1u) ready = ld_acquire_sys(tok_counter(me, d, ph, a.par, (int)t)) >= need;
+      if ((todo >> lane) & 1u) ready = ld_acquire_sys(tok_counter(me, d, ph, PAR(a), (int)t)) >= need;
       unsigned r = __ballot_sync(0xffffffffu, ready);
       if (!r) {
         if (aborted(a.err)) return;
@@ -781,7 +792,7 @@ struct ModeUp {
   }
   __device__ static void before_loads(const Args& a, const TileDesc& td) {
     const SymPtrs& me = a.peers.p[a.d.rank];
-    wait_geq_sys(rg_counter(me, a.d, 0, a.par, td.m0 >> 7), (uint32_t)td.rows, a.timeout_ns, a.err,
+    wait_geq_sys(rg_counter(me, a.d, 0, PAR(a), td.m0 >> 7), (uint32_t)td.rows, a.timeout_ns, a.err,
                  30, td.m0 >> 7);
   }
   __device__ static void epilogue_prefetch(const Args&, const TileDesc&, int) {}
@@ -866,7 +877,7 @@ __device__ __forceinline__ void push_rows(const MkArgs& a, const TileDesc& td, u
     acc_chunk(taddr, c, v);
     if (live) store_row_bf16_32(dst + c * 32, v);
   }
-  if (live) red_release_sys_add(tok_counter(S, a.d, ph, a.par, mt.rep / a.d.topk), 1u);
+  if (live) red_release_sys_add(tok_counter(S, a.d, ph, PAR(a), mt.rep / a.d.topk), 1u);
 }
 
 // Forward down projection + combine push: A = hact (K-major over F), B = W_down (K-major).
@@ -991,7 +1002,7 @@ struct ModeDgradDown {
   __device__ static void before_loads(const Args& a, const TileDesc& td) {
     if (!td.pad1) {
       const SymPtrs& me = a.peers.p[a.d.rank];
-      wait_geq_sys(rg_counter(me, a.d, 1, a.par, td.m0 >> 7), (uint32_t)td.rows, a.timeout_ns,
+      wait_geq_sys(rg_counter(me, a.d, 1, PAR(a), td.m0 >> 7), (uint32_t)td.rows, a.timeout_ns,
                    a.err, 31, td.m0 >> 7);
     } else {
       wait_geq_sys(a.wg_cnt + td.e * (a.d.F / BN) + td.pad0, (uint32_t)a.p.mblocks[td.e],
@@ -1223,16 +1234,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const bool has_pre = (KIND == 0 || KIND == 2);
   const bool has_post = (KIND == 1 || KIND == 3);
 
+  load_epoch(a);
   // Reset the other parity of this phase's counters (used one iteration ago, all their
   // increments have landed) -- see DESIGN.md §Scoreboard.
   if (blockIdx.x == 0) {
     const SymPtrs& me = a.peers.p[a.d.rank];
     if (has_pre)
       for (int g = threadIdx.x; g < a.d.RG_cap; g += blockDim.x)
-        *rg_counter(me, a.d, ph, a.par ^ 1, g) = 0;
+        *rg_counter(me, a.d, ph, (PAR(a) ^ 1), g) = 0;
     if (has_post)
       for (int t = threadIdx.x; t < a.d.T_max; t += blockDim.x)
-        *tok_counter(me, a.d, ph, a.par ^ 1, t) = 0;
+        *tok_counter(me, a.d, ph, (PAR(a) ^ 1), t) = 0;
   }
   gemm_setup(S);
 
@@ -1300,12 +1312,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int ph = (KIND >= 2) ? 1 : 0;
   const bool has_pre = (KIND == 0 || KIND == 2);
   const bool has_post = (KIND == 1 || KIND == 3);
+  load_epoch(a);
   if (blockIdx.x == 0) {
     const SymPtrs& me = a.peers.p[a.d.rank];
     if (has_pre)
-      for (int g = threadIdx.x; g < a.d.RG_cap; g += blockDim.x) *rg_counter(me, a.d, ph, a.par ^ 1, g) = 0;
+      for (int g = threadIdx.x; g < a.d.RG_cap; g += blockDim.x) *rg_counter(me, a.d, ph, (PAR(a) ^ 1), g) = 0;
     if (has_post)
-      for (int t = threadIdx.x; t < a.d.T_max; t += blockDim.x) *tok_counter(me, a.d, ph, a.par ^ 1, t) = 0;
+      for (int t = threadIdx.x; t < a.d.T_max; t += blockDim.x) *tok_counter(me, a.d, ph, (PAR(a) ^ 1), t) = 0;
   }
   gemm_setup_pair(S, rank);
   const int n_pre = has_pre ? a.n_disp + a.n_relay : 0;

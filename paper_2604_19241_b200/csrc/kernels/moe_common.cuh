@@ -128,8 +128,7 @@ struct MkArgs {
   uint32_t* wg_cnt;             // [epr][F/256] down-dgrad tiles done (zeroed per bwd call)
   int* cursor;
   int* err;
-  uint32_t epoch;               // iteration number (>= 1)
-  int par;                      // epoch & 1
+  const uint32_t* epoch_dev;    // device iteration counter (>= 1), advanced by plan_global_kernel
   int n_disp, n_relay, n_red;
   unsigned long long timeout_ns;
   Timeline tl;

@@ -25,9 +25,19 @@ __global__ void plan_hist_kernel(const int* __restrict__ ids, int n, int E, int*
   for (int e = threadIdx.x; e < E; e += blockDim.x) hist[(size_t)blockIdx.x * E + e] = h[e];
 }
 
-__global__ void plan_global_kernel(Dims d, Peers peers, PlanDev p, int nchunks, uint32_t epoch,
+__global__ void plan_global_kernel(Dims d, Peers peers, PlanDev p, int nchunks, uint32_t* epoch_dev,
                                    uint64_t timeout_ns, int* err) {
   const int E = d.E, W = d.world, epr = d.epr, me = d.rank;
+  // a new iteration: advance the device epoch (every MegaKernel of the iteration reads it, so a
+  // captured graph of plan + MegaKernels replays with fresh flags and counter parities)
+  __shared__ uint32_t epoch_s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    epoch_s = *epoch_dev + 1;
+    *epoch_dev = epoch_s;
+  }
+  __syncthreads();
+  const uint32_t epoch = epoch_s;
   __shared__ int rt[MAX_EXPERTS];   // recv totals per (dst, e_loc) = global expert
   __shared__ int cnt_s[MAX_EXPERTS];
   // (a) CumSum over chunks (chunk bases) and C_exp
@@ -192,7 +202,7 @@ __global__ void zero_padding_kernel(Dims d, PlanDev p, __nv_bfloat16* recv) {
 namespace eplab_launch {
 using namespace eplab_dev;
 
-int plan_launch(const Dims& d, const Peers& peers, const PlanDev& p, uint32_t epoch,
+int plan_launch(const Dims& d, const Peers& peers, const PlanDev& p, uint32_t* epoch,
                 uint64_t timeout_ns, int* err, cudaStream_t st) {
   const int n = p.n_tok * d.topk;
   const int nchunks = n > 0 ? (n + PLAN_CHUNK - 1) / PLAN_CHUNK : 0;

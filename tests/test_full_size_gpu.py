@@ -65,3 +65,65 @@ def test_full_size_parity(cfg):
     assert_close(bf16_to_f32(to_u16(a["dx"][toks])).reshape(-1), bf16_to_f32(ref["dx"]).reshape(-1), "dx")
     assert_close(a["dgate"][toks].cpu().numpy().reshape(-1), ref["dgate"].reshape(-1), "dgate")
     layer.close()
+
+
+@pytest.mark.parametrize("relay", [0, 4])
+def test_world_invariance_full_size_qwen3_ep8(relay):
+    """Qwen3 shape (128 experts, top-8, H 2048, F 768) with 16K tokens per rank on 8 virtual
+    ranks (one process, 18 SMs each, peer rows through the same symmetric buffers the NVLink path
+    uses) equals EP=1 on the same 131K tokens bit for bit -- y, dx, dgate, dW -- with the
+    AllToAll-style (relay off) and AllGather-style (relay on) dispatch."""
+    from paper_2604_19241_b200 import moe as M
+    from paper_2604_19241_b200.model import sample_routing
+    H, F, E, k, T = SHAPES["qwen3"]
+    W = 8
+    sel, gw = sample_routing(E, k, T, W, 3)  # [W][T*k]: rank r's tokens are global tokens r*T..
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(W * T, H, device="cuda", generator=g).bfloat16()
+    dy = (torch.randn(W * T, H, device="cuda", generator=g) * 0.5).bfloat16()
+    w_up = (torch.randn(E, 2 * F, H, device="cuda", generator=g) * H ** -0.5).bfloat16()
+    w_down = (torch.randn(E, H, F, device="cuda", generator=g) * F ** -0.5).bfloat16()
+    ids = torch.from_numpy(sel.reshape(W * T, k).copy()).cuda()
+    gws = torch.from_numpy(gw.reshape(W * T, k).copy()).cuda()
+    # EP=1 over all W*T tokens
+    one = M.EpMoE(H, F, E, k, W * T, max_recv_rows=W * T * k)
+    y1 = one.forward(x, ids, gws, w_up, w_down)
+    g1 = one.backward(dy, w_up, w_down)
+    one.check()
+    torch.cuda.synchronize()
+    one.close()
+    # EP=8: 16 experts and T tokens per virtual rank (receive capacity for balanced routing + slack)
+    epr = E // W
+    ranks = [M.EpMoE(H, F, E, k, T, rank=r, world=W, max_recv_rows=T * k * 5 // 4, timeout_s=60.0)
+             for r in range(W)]
+    M.EpMoE.connect_local(ranks)
+    for r in ranks:
+        r.set_sm_budget(148 // W)
+        r.set_tune_config((4, relay, 1, 148 // W, 8))
+    streams = [torch.cuda.Stream() for _ in range(W)]
+    torch.cuda.synchronize()
+    ys, gs = [None] * W, [None] * W
+    for ph in range(3):
+        for r in range(W):
+            sl = slice(r * T, (r + 1) * T)
+            with torch.cuda.stream(streams[r]):
+                if ph == 0:
+                    ranks[r].plan(ids[sl], gws[sl], streams[r])
+                elif ph == 1:
+                    ranks[r].dispatch_group_gemm(x[sl], w_up[r * epr:(r + 1) * epr], streams[r])
+                    ys[r] = ranks[r].group_gemm_combine(w_down[r * epr:(r + 1) * epr], stream=streams[r])
+                else:
+                    gs[r] = ranks[r].backward(dy[sl], w_up[r * epr:(r + 1) * epr],
+                                              w_down[r * epr:(r + 1) * epr], stream=streams[r])
+        if ph == 0:
+            torch.cuda.synchronize()
+    for r in range(W):
+        ranks[r].check(streams[r])
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(ys), y1), "y"
+    assert torch.equal(torch.cat([gg["dx"] for gg in gs]), g1["dx"]), "dx"
+    assert torch.equal(torch.cat([gg["dgate"] for gg in gs]), g1["dgate"]), "dgate"
+    assert torch.equal(torch.cat([gg["dw_up"] for gg in gs]), g1["dw_up"]), "dw_up"
+    assert torch.equal(torch.cat([gg["dw_down"] for gg in gs]), g1["dw_down"]), "dw_down"
+    for r in ranks:
+        r.close()

@@ -142,6 +142,7 @@ MkArgs base_args(eplab_ctx* c) {
   a.comm_bulk = c->comm_bulk;
   a.comm_cursor = c->cursor + 2;
   a.red_cursor = reinterpret_cast<unsigned*>(c->cursor + 4);
+  a.relay_cursor = reinterpret_cast<unsigned*>(c->cursor + 5);
   a.spare_warps = c->spare_warps;
   // A/B experiments: environment switches read per launch
   if (const char* e = getenv("EPLAB_COMM")) a.comm_bulk = std::string(e) == "bulk";

@@ -603,40 +603,102 @@ __device__ void comm_task(const MkArgs& a, int task, int ph, GemmSmem* S, uint8_
 }
 
 // ------------------------------------------------------------------ relay role
-// Owns whole destination rowgroups (even split, sim.cpp:236-238); copies every duplicate
-// replica from its primary slot in HBM, then publishes the rowgroup count.
-__device__ void relay_task(const MkArgs& a, int task, int ph) {
+// Relay workers (relay on; sim.cpp:418-441) are a pool of destination
+// rowgroups claimed in order by warps -- the n_relay relay CTAs' 8 warps and, after the comm
+// pool is drained, the GEMM CTAs' spare warps. A warp takes a whole rowgroup: each lane polls the
+// metadata flags of its slots (and, for duplicates, the primary slot's row flag), the warp copies
+// every duplicate from its primary slot in HBM (two rows in flight), then publishes the rowgroup
+// count (sim.cpp:601-618).
+__device__ void relay_rowgroup(const MkArgs& a, int ph, int g) {
   const Dims& d = a.d;
   const SymPtrs& me = a.peers.p[d.rank];
-  const int n_rg = a.p.scalars[1];
-  long long g0, g1;
-  even_slice(n_rg, a.n_relay, task, g0, g1);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
   const uint32_t flagv = EPOCH(a) * 2 + ph;
-  __nv_bfloat16* recv = ph == 0 ? me.recv_x : me.recv_dy;
+  const int4* recv = reinterpret_cast<const int4*>(ph == 0 ? me.recv_x : me.recv_dy);
+  int4* recv_w = reinterpret_cast<int4*>(ph == 0 ? me.recv_x : me.recv_dy);
   const int vecs = d.H / 8;
-  for (long long g = g0; g < g1; ++g) {
-    const int el = expert_of_block(a.p, d.epr, g);
-    const int ge = d.rank * d.epr + el;
-    const int rows = min(BM, a.p.rt_all[ge] - (int)(g - a.p.mblock_pre[el]) * BM);
-    for (int r = warp; r < rows; r += GEMM_THREADS / 32) {
-      const int s = (int)g * BM + r;
-      if (lane == 0) wait_eq_sys(me.slot_flag + s, flagv, a.timeout_ns, a.err, 10 + ph, s);
-      __syncwarp();
-      const int prim = me.meta[s].primary;
-      if (prim >= 0 && lane == 0) wait_eq_sys(me.slot_flag + prim, flagv, a.timeout_ns, a.err, 12 + ph, prim);
-      __syncwarp();
-      if (prim >= 0)
-        warp_copy_row<8>(reinterpret_cast<int4*>(recv + (size_t)s * d.H),
-                         reinterpret_cast<const int4*>(recv + (size_t)prim * d.H), vecs, lane);
+  const int el = expert_of_block(a.p, d.epr, g);
+  const int ge = d.rank * d.epr + el;
+  const int rows = min(BM, a.p.rt_all[ge] - (g - a.p.mblock_pre[el]) * BM);
+  for (int r0 = 0; r0 < rows; r0 += 32) {
+    const int s = g * BM + r0 + lane;
+    const bool live = r0 + lane < rows;
+    int prim = -1;
+    // lane-parallel waits: metadata flag of my slot, then (duplicate) the primary's row flag
+    const unsigned long long t0 = globaltimer();
+    bool ok = !live;
+    while (!__all_sync(0xffffffffu, ok)) {
+      if (!ok) {
+        if (prim < 0 && ld_acquire_sys(me.slot_flag + s) == flagv) {
+          prim = me.meta[s].primary;  // >= 0: a duplicate -- wait for its primary's row
+          ok = prim < 0;
+        }
+        if (prim >= 0 && ld_acquire_sys(me.slot_flag + prim) == flagv) ok = true;
+      }
+      const bool late = globaltimer() - t0 > a.timeout_ns;
+      if (__any_sync(0xffffffffu, aborted(a.err) || late)) {  // warp-uniform exit
+        if (late && !ok) report_timeout(a.err, 10 + ph, flagv, 0, s);
+        return;
+      }
+      // back off between polls: hundreds of lanes spinning on acquire loads starve the comm
+      // rounds and GEMM producers sharing L2 (measured: EP=2 relay dispatch 7 ms -> <1 ms)
+      if (!__all_sync(0xffffffffu, ok)) __nanosleep(200);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      red_release_gpu_add(rg_counter(me, d, ph, PAR(a), (int)g), (uint32_t)rows);
+    unsigned m = __ballot_sync(0xffffffffu, live && prim >= 0);
+    while (m) {
+      const int qa = __ffs(m) - 1;
+      m &= m - 1;
+      const int qb = m ? __ffs(m) - 1 : qa;
+      if (m) m &= m - 1;
+      const bool two = qb != qa;
+      const int pa = __shfl_sync(0xffffffffu, prim, qa), pb = __shfl_sync(0xffffffffu, prim, qb);
+      const int4* sa = recv + (size_t)pa * vecs;
+      const int4* sb = recv + (size_t)pb * vecs;
+      int4* da = recv_w + (size_t)(g * BM + r0 + qa) * vecs;
+      int4* db = recv_w + (size_t)(g * BM + r0 + qb) * vecs;
+      for (int c = lane; c < vecs; c += 256) {
+        int4 va[8], vb[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (c + 32 * u < vecs) {
+            va[u] = sa[c + 32 * u];
+            if (two) vb[u] = sb[c + 32 * u];
+          }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (c + 32 * u < vecs) {
+            da[c + 32 * u] = va[u];
+            if (two) db[c + 32 * u] = vb[u];
+          }
+      }
     }
   }
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    red_release_gpu_add(rg_counter(me, d, ph, PAR(a), g), (uint32_t)rows);
+  }
 }
+
+// A relay worker warp: claim rowgroups until the pool is empty. Returns the number handled.
+__device__ int relay_rowgroups(const MkArgs& a, int ph) {
+  const int n_rg = a.p.scalars[1];
+  const int lane = threadIdx.x & 31;
+  int done = 0;
+  for (;;) {
+    int g = 0;
+    if (lane == 0) g = (int)atomicAdd(a.relay_cursor, 1u);
+    g = __shfl_sync(0xffffffffu, g, 0);
+    if (g >= n_rg) break;
+    const unsigned long long t0 = globaltimer();
+    relay_rowgroup(a, ph, g);
+    if (lane == 0 && (a.dbg & 128)) timeline_push(a.tl, t0, globaltimer(), ROLE_RELAY, 100000 + g);
+    ++done;
+  }
+  return done;
+}
+
+__device__ void relay_task(const MkArgs& a, int, int ph) { relay_rowgroups(a, ph); }
 
 // ------------------------------------------------------------------ reduce role
 // Top-k completeness barrier, then the fixed k-ascending fold (
@@ -735,7 +797,7 @@ __device__ void reduce_chunks_t(const MkArgs& a, int ph, bool backoff) {
           if (lane == 0) report_timeout(a.err, 20 + ph, need, 0, (int)(c * RCHUNK + __ffs(todo) - 1));
           return;
         }
-        if (backoff) __nanosleep(500);
+        if (backoff) __nanosleep(500);  // (post-task pollers must not sleep: 100 ns costs 0.1-0.4 ms)
         continue;
       }
       todo &= ~r;
@@ -775,9 +837,15 @@ __device__ __forceinline__ void spare_reduce(const MkArgs& a, const Timeline& tl
 // their activity goes into the device timeline as one comm interval per warp.
 __device__ __forceinline__ void spare_comm(const MkArgs& a, const Timeline& tl, int ph) {
   if (!(a.spare_warps & 1) || a.comm_bulk) return;
-  const unsigned long long t0 = globaltimer();
+  unsigned long long t0 = globaltimer();
   const int n = comm_rounds(a, ph);
   if (n > 0 && (threadIdx.x & 31) == 0) timeline_push(tl, t0, globaltimer(), ROLE_COMM, -1 - (int)(threadIdx.x >> 5));
+  if (a.n_relay > 0) {  // then the relay pool (it waits on rows; the comm pool never waits)
+    t0 = globaltimer();
+    const int nr = relay_rowgroups(a, ph);
+    if (nr > 0 && (threadIdx.x & 31) == 0)
+      timeline_push(tl, t0, globaltimer(), ROLE_RELAY, -1 - (int)(threadIdx.x >> 5));
+  }
 }
 
 struct ModeUp {
@@ -1380,7 +1448,7 @@ using namespace eplab_dev;
 template <int KIND, class Mode>
 static int launch_mk(const TmaSet& tm, const MkArgs& a, int grid, cudaStream_t st) {
   static bool attr = false, attr_p = false;
-  cudaMemsetAsync(a.cursor, 0, 32, st);  // task cursor, comm round counter, reduce chunk counter
+  cudaMemsetAsync(a.cursor, 0, 32, st);  // task cursor, comm rounds, reduce chunks, relay rowgroups
   if (!a.pair) {
     auto fn = megakernel<KIND, Mode>;
     if (!attr) {

@@ -136,7 +136,8 @@ struct MkArgs {
             // 16 = skip the saved g, u loads of the dgrad epilogue
   int pair;  // 1: CTA-pair (cta_group::2) engine
   int* comm_cursor;  // [2] u64 round counter of the comm pool (zeroed per launch with cursor)
-  unsigned* red_cursor;  // reduce chunk counter (zeroed per launch with cursor)
+  unsigned* red_cursor;    // reduce chunk counter (zeroed per launch with cursor)
+  unsigned* relay_cursor;  // relay rowgroup counter (zeroed per launch with cursor)
   int spare_warps;  // bit 0: the GEMM CTAs' spare warps join the comm pool (warp split),
                     // bit 1: ... and the backward combine's reduce pool
   int comm_bulk;

@@ -15,6 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="qwen3")
 ap.add_argument("--relay", type=int, default=0)
 ap.add_argument("--steps", type=int, default=5)
+ap.add_argument("--trace", type=int, default=0, help="EP size whose rank-0 fwd dispatch is traced")
 args = ap.parse_args()
 H, F, E, k, T_all = bench.CONFIGS[args.config]
 g = torch.Generator(device="cuda").manual_seed(5)
@@ -83,6 +84,20 @@ for W in (1, 2, 4, 8):
     torch.cuda.synchronize()
     for r in range(W):
         ranks[r].check(streams[r])
+    if args.trace == W:
+        ranks[0].timeline_enable(1 << 20)
+        for ph in range(2):
+            for r in range(W):
+                sl = slice(r * T, (r + 1) * T)
+                with torch.cuda.stream(streams[r]):
+                    if ph == 0:
+                        ranks[r].plan(ids[sl], gws[sl], streams[r])
+                    else:
+                        ranks[r].dispatch_group_gemm(x[sl], w_up[r * epr:(r + 1) * epr], streams[r])
+        torch.cuda.synchronize()
+        os.makedirs("gpurun_out", exist_ok=True)
+        ranks[0].timeline_export(f"gpurun_out/vep_trace_{args.config}_ep{W}_relay{args.relay}.json")
+        ranks[0].timeline_enable(0)
     ms = e0.elapsed_time(e1) / args.steps
     step(rec=True)
     torch.cuda.synchronize()

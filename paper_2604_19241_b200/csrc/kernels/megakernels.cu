@@ -412,7 +412,10 @@ __device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
     const unsigned rel = copied & ~done;
     if (!rel) return;
     __syncwarp();
-    fence_acq_rel_sys();
+    if (d.world == 1)
+      fence_acq_rel_gpu();  // one GPU: every reader is on this device
+    else
+      fence_acq_rel_sys();
     const bool mine = (rel >> lane) & 1u;
     if (a.n_relay > 0) {
       if (mine) st_relaxed_sys(a.peers.p[dst].slot_flag + slot, EPOCH(a) * 2 + ph);
@@ -945,7 +948,13 @@ __device__ __forceinline__ void push_rows(const MkArgs& a, const TileDesc& td, u
     acc_chunk(taddr, c, v);
     if (live) store_row_bf16_32(dst + c * 32, v);
   }
-  if (live) red_release_sys_add(tok_counter(S, a.d, ph, PAR(a), mt.rep / a.d.topk), 1u);
+  if (live) {
+    uint32_t* ctr = tok_counter(S, a.d, ph, PAR(a), mt.rep / a.d.topk);
+    if (a.d.world == 1)
+      red_release_gpu_add(ctr, 1u);  // one GPU: the reducer is on this device
+    else
+      red_release_sys_add(ctr, 1u);
+  }
 }
 
 // Forward down projection + combine push: A = hact (K-major over F), B = W_down (K-major).

@@ -226,6 +226,9 @@ __device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
 __device__ __forceinline__ void fence_acq_rel_sys() {
   asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 
 // 16-byte streaming load / store (L1 no-allocate) for row copies.
 __device__ __forceinline__ int4 ld_nc_v4(const int4* p) {

@@ -957,11 +957,18 @@ __device__ __forceinline__ void push_rows(const MkArgs& a, const TileDesc& td, u
   }
 }
 
+// Pull this row's slot metadata (return address / gate weight) into L1 before the accumulator
+// is ready, so the epilogue's first dependent load does not wait on L2.
+__device__ __forceinline__ void prefetch_meta_l1(const MkArgs& a, const TileDesc& td, int r) {
+  if (td.pad1 || r >= td.rows) return;
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(a.peers.p[a.d.rank].meta + td.m0 + r));
+}
+
 // Forward down projection + combine push: A = hact (K-major over F), B = W_down (K-major).
 struct ModeDown {
   using Args = MkArgs;
   static constexpr bool HAS_TILE_DONE = false;
-  __device__ static void epilogue_prefetch(const Args&, const TileDesc&, int) {}
+  __device__ static void epilogue_prefetch(const Args& a, const TileDesc& td, int r) { prefetch_meta_l1(a, td, r); }
   __device__ static TileDesc tile_pair(const Args& a, int t) {
     return nt_tile_pair(a.d, a.p, t, a.d.H / BN, BN, a.d.F / BK, a.rgp);
   }
@@ -1090,6 +1097,7 @@ struct ModeDgradDown {
   // accumulator is ready
   __device__ static void epilogue_prefetch(const Args& a, const TileDesc& td, int r) {
     if (td.pad1 || r >= td.rows) return;
+    prefetch_meta_l1(a, td, r);
     const char* g = reinterpret_cast<const char*>(a.gu + ((size_t)td.m0 + r) * 2 * a.d.F + td.n0);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -1229,7 +1237,7 @@ struct ModeDgradUp {
   static constexpr bool HAS_TILE_DONE = false;
   static constexpr bool SPARE = true;
   __device__ static void spare(const Args& a, const Timeline& tl) { spare_reduce(a, tl, 1); }
-  __device__ static void epilogue_prefetch(const Args&, const TileDesc&, int) {}
+  __device__ static void epilogue_prefetch(const Args& a, const TileDesc& td, int r) { prefetch_meta_l1(a, td, r); }
   __device__ static int n_dgrad_pair(const Args& a) { return a.p.mpair_pre[a.d.epr] * (a.d.H / BN); }
   __device__ static TileDesc tile_pair(const Args& a, int t) {
     const int nd = n_dgrad_pair(a);

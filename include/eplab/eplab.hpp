@@ -164,14 +164,14 @@ struct B200Calib {
   // fitted over 76 measured cases (tools/fit_model.py, profiles/r01_perf_model_validation.md)
   double mu = 1.0;                // tensor-pipe efficiency of the tile main loop vs p_peak (sustained)
   double tile_overhead = 0.2e-6;  // per-tile hand-off cost not hidden behind the loop, s
-  double comm_bw_per_sm = 46.2e9; // B/s one comm CTA sustains (8 warps of warp copies)
-  double relay_bw_per_sm = 46.2e9;  // B/s one relay CTA sustains on HBM copies
-  double reduce_bw = 4.247e12;    // B/s of the reduce role when all SMs join
-  double launch = 49.35e-6;       // per MegaKernel fixed cost: launch, prologue, pipeline fill
-  double epi_bw_per_sm = 196.8e9; // B/s of epilogue traffic per SM (TMA stores, saved-input reads)
-  double spare_sm_equiv = 25.89;  // comm capacity of the GEMM CTAs' spare warps, in comm-CTA units
+  double comm_bw_per_sm = 25.01e9; // B/s one comm CTA sustains (8 warps of warp copies)
+  double relay_bw_per_sm = 25.01e9;  // B/s one relay CTA sustains on HBM copies
+  double reduce_bw = 6.5e12;      // B/s of the reduce role when all SMs join
+  double launch = 42.19e-6;       // per MegaKernel fixed cost: launch, prologue, pipeline fill
+  double epi_bw_per_sm = 200.0e9; // B/s of epilogue traffic per SM (TMA stores, saved-input reads)
+  double spare_sm_equiv = 41.78;  // comm capacity of the GEMM CTAs' spare warps, in comm-CTA units
                                   // (0: spare warps off / not modelled)
-  double hbm_overlap = 0.619;     // kernel time = max(compute, HBM) + hbm_overlap * min(compute, HBM)
+  double hbm_overlap = 0.513;     // kernel time = max(compute, HBM) + hbm_overlap * min(compute, HBM)
                                   // (HBM = the kernel's algorithmic bytes at bw_hbm)
 };
 struct LayerPrediction {

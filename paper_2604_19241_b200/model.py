@@ -51,7 +51,7 @@ class LayerPrediction(C.Structure):
 
 # B200 calibration of this build (DESIGN.md §Performance model; refit by tools/calibrate_model.py)
 # fitted over 76 measured cases, spare-warp comm workers on/off (profiles/r01_perf_model_validation.md)
-B200_CALIB = Calib(1.0, 0.2e-6, 46.2e9, 46.2e9, 4.247e12, 49.35e-6, 196.8e9, 25.89, 0.619)
+B200_CALIB = Calib(1.0, 0.2e-6, 25.01e9, 25.01e9, 6.5e12, 42.19e-6, 200.0e9, 41.78, 0.513)
 
 
 def hw(world, n_sm=148, p_peak=1408.1e12, bw_hbm=6468.9e9, bw_nvl=770e9, w_sat=1024.0, tau_sync=1e-6):

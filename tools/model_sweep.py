@@ -25,7 +25,7 @@ def measure(H, F, E, k, T, cfg, steps=3, spare=1):
     w_down = (torch.randn(E, H, F, device="cuda", generator=g) * F ** -0.5).bfloat16()
     L = M.EpMoE(H, F, E, k, T)
     L.set_tune_config(cfg)
-    L.set_comm_options(spare_warps=bool(spare))
+    L.set_comm_options(spare_warps=3 if spare else 0)
     y = torch.empty(T, H, device="cuda", dtype=torch.bfloat16)
     out = dict(dx=torch.empty(T, H, dtype=torch.bfloat16, device="cuda"), dw_up=torch.empty_like(w_up),
                dw_down=torch.empty_like(w_down), dgate=torch.empty(T, k, dtype=torch.float32, device="cuda"))

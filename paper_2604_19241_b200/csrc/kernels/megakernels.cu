@@ -950,7 +950,9 @@ __device__ __forceinline__ void push_rows(const MkArgs& a, const TileDesc& td, u
   }
   if (live) {
     uint32_t* ctr = tok_counter(S, a.d, ph, PAR(a), mt.rep / a.d.topk);
-    if (a.d.world == 1)
+    if (a.dbg & 256)
+      red_relaxed_sys_add(ctr, 1u);  // experiment only: no release ordering (measures the fence)
+    else if (a.d.world == 1)
       red_release_gpu_add(ctr, 1u);  // one GPU: the reducer is on this device
     else
       red_release_sys_add(ctr, 1u);

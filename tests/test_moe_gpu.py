@@ -258,6 +258,9 @@ def test_empty_batch_and_validation_errors():
     with pytest.raises(m.EplabError) as e:  # deadlock constraint of validate_tune_config
         layer.set_tune_config((140, 10, 1, 148, 8))
     assert e.value.code == 2
+    with pytest.raises(m.EplabError) as e:  # spare-warp roles are a 2-bit set
+        layer.set_comm_options(spare_warps=4)
+    assert e.value.code == 2
     with pytest.raises(m.EplabError):
         m.EpMoE(300, 256, 8, 2, 64)  # hidden not a multiple of 256
     layer.close()

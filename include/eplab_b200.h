@@ -129,6 +129,10 @@ EPLAB_API int eplab_connect_local(eplab_ctx* const* ctxs, int n);
 
 EPLAB_API int eplab_set_tune_config(eplab_ctx* ctx, const eplab_tune_config* cfg);
 EPLAB_API int eplab_get_tune_config(const eplab_ctx* ctx, eplab_tune_config* cfg);
+/* Auto-tune (the default until eplab_set_tune_config is called): every eplab_plan picks the launch
+ * parameters for its n_tok from the B200 performance model (search_layer), cached per 4096-token
+ * bucket as the reference TuneCache does (tuner.hpp:60). on = 1 re-enables it (clears the cache). */
+EPLAB_API int eplab_set_auto_tune(eplab_ctx* ctx, int on);
 /* Work for the GEMM CTAs' idle warps (the unified primitive's warp split), a bit set:
  * bit 0 (comm): they drain the dispatch MegaKernels' priority-ordered round pool together with
  * the n_disp comm CTAs, so n_disp may be 0; bit 1 (reduce): they fold completed dX tokens in the

@@ -7,10 +7,12 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <map>
 #include <sstream>
 #include <string>
 #include <vector>
 
+#include "eplab/eplab.hpp"
 #include "eplab_b200.h"
 #include "host/errors.hpp"
 #include "host/launch.hpp"
@@ -78,6 +80,10 @@ struct eplab_ctx {
   // comm pool workers: spare GEMM warps join (warp split; EPLAB_SPARE=0 disables), bulk-copy
   // mover instead of warp copies (EPLAB_COMM=bulk); eplab_set_comm_options overrides both
   int spare_warps = 3, comm_bulk = 0;
+  // auto-tune (default until eplab_set_tune_config): per 4096-token bucket of n_tok, the
+  // B200 model's search_layer result (the reference TuneCache's bucketing, tuner.cpp:150-165)
+  bool auto_tune = true;
+  std::map<long long, eplab_tune_config> tune_cache;
   // timeline
   TimelineRec* tl_rec = nullptr;
   int* tl_count = nullptr;
@@ -376,6 +382,7 @@ int eplab_set_tune_config(eplab_ctx* c, const eplab_tune_config* cfg) {
              "n_disp + n_relay must be < n_sm (deadlock constraint)");
     validate(cfg->n_red >= 1 && cfg->n_red <= c->num_sms, "n_red must be in [1, n_sm]");
     c->cfg = *cfg;
+    c->auto_tune = false;
   });
 }
 
@@ -385,6 +392,7 @@ int eplab_set_sm_budget(eplab_ctx* c, int n_sm) {
     CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device));
     validate(n_sm >= 2 && n_sm <= dev_sms, "sm budget must be in [2, device SMs]");
     c->num_sms = n_sm;
+    c->tune_cache.clear();
     c->cfg.n_red = std::min(c->cfg.n_red, n_sm);
     if (c->cfg.n_disp + c->cfg.n_relay >= n_sm) {
       c->cfg.n_disp = std::max(1, n_sm / 4);
@@ -399,6 +407,7 @@ int eplab_set_comm_options(eplab_ctx* c, int spare_warps, int bulk_mover) {
     validate(bulk_mover == 0 || bulk_mover == 1, "bulk_mover must be 0 or 1");
     c->spare_warps = spare_warps;
     c->comm_bulk = bulk_mover;
+    c->tune_cache.clear();
   });
 }
 
@@ -407,9 +416,63 @@ int eplab_get_tune_config(const eplab_ctx* c, eplab_tune_config* cfg) {
   return EPLAB_OK;
 }
 
+namespace {
+// Launch parameters for this context's shape at n_tok tokens per rank: search_layer over the B200
+// model at the bucket's upper edge, n_red = every SM, and the measured floor on comm CTAs the model
+// does not capture (16 with the spare-warp comm workers, 64 without, scaled by the SM budget;
+// profiles/r01_spare_warps.txt). Cached per 4096-token bucket.
+eplab_tune_config search_config(eplab_ctx* c, long long bucket);
+
+eplab_tune_config auto_config(eplab_ctx* c, int n_tok) {
+  const long long bucket = eplab::token_bucket(std::max(1, n_tok));
+  auto it = c->tune_cache.find(bucket);
+  if (it != c->tune_cache.end()) return it->second;
+  eplab_tune_config cfg = search_config(c, bucket);
+  if (c->d.world > 1) {
+    // relay on/off is a protocol choice every rank must share (a sender's dedup needs the
+    // receiver's relay): take it from the max_tokens bucket, identical on every rank; only the
+    // SM split follows this rank's n_tok
+    const eplab_tune_config ref = search_config(c, eplab::token_bucket(c->d.T_max));
+    if ((ref.n_relay > 0) != (cfg.n_relay > 0)) {
+      cfg.n_relay = ref.n_relay;
+      if (cfg.n_disp + cfg.n_relay >= c->num_sms) cfg.n_disp = ref.n_disp;
+    }
+  }
+  c->tune_cache[bucket] = cfg;
+  return cfg;
+}
+
+eplab_tune_config search_config(eplab_ctx* c, long long bucket) {
+  eplab::MoEShape shape;
+  shape.name = "ctx";
+  shape.h_dim = c->d.H;
+  shape.h_inter = c->d.F;
+  shape.n_exp = c->d.E;
+  shape.topk = c->d.topk;
+  shape.n_tok = bucket * 4096;
+  eplab::HardwareSpec hw = eplab::b200_hardware(c->d.world);
+  hw.n_sm = c->num_sms;
+  eplab::B200Calib calib;
+  if (!(c->spare_warps & 1)) calib.spare_sm_equiv = 0;
+  const eplab::TuneResult r = eplab::search_layer(hw, shape, 0, calib);
+  eplab_tune_config cfg{r.best.n_disp, r.best.n_relay, 1, c->num_sms, 8};
+  const int floor = ((c->spare_warps & 1) ? 16 : 64) * c->num_sms / 148;
+  if (cfg.n_disp < floor && floor + cfg.n_relay < c->num_sms) cfg.n_disp = floor;
+  return cfg;
+}
+}  // namespace
+
+int eplab_set_auto_tune(eplab_ctx* c, int on) {
+  return guarded([&] {
+    c->auto_tune = on != 0;
+    c->tune_cache.clear();
+  });
+}
+
 int eplab_plan(eplab_ctx* c, const int32_t* ids, const float* gw, int n_tok, void* stream) {
   return guarded([&] {
     validate(n_tok >= 0 && n_tok <= c->d.T_max, "n_tok exceeds max_tokens");
+    if (c->auto_tune) c->cfg = auto_config(c, n_tok);
     CK(cudaSetDevice(c->device));
     cudaStream_t st = (cudaStream_t)stream;
     c->epoch++;

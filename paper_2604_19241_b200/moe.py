@@ -48,6 +48,7 @@ _SIGS = {
     "eplab_get_tune_config": [_P, C.POINTER(TuneConfig)],
     "eplab_set_sm_budget": [_P, _I],
     "eplab_set_comm_options": [_P, _I, _I],
+    "eplab_set_auto_tune": [_P, _I],
     "eplab_plan": [_P, _P, _P, _I, _P],
     "eplab_dispatch_group_gemm": [_P, _P, _P, _P],
     "eplab_group_gemm_combine": [_P, _P, _P, _P],
@@ -166,6 +167,11 @@ class EpMoE:
         """spare_warps: bit 0 = comm pool, bit 1 = backward reduce pool (True = 3, False = 0)."""
         sw = 3 if spare_warps is True else (0 if spare_warps is False else int(spare_warps))
         _check(lib().eplab_set_comm_options(self.h, sw, int(bulk_mover)))
+
+    def set_auto_tune(self, on=True):
+        """Per-plan launch parameters from the B200 model, cached per 4096-token bucket (default
+        until set_tune_config)."""
+        _check(lib().eplab_set_auto_tune(self.h, int(on)))
 
     def tune_config(self):
         c = TuneConfig()

@@ -418,3 +418,27 @@ def test_cuda_graph_replay_matches_eager():
         for key in ref:
             assert torch.equal(got[key], ref[key]), f"graph replay {key}"
     L.close()
+
+
+def test_auto_tune_per_token_bucket():
+    """Without an explicit TuneConfig every plan takes the B200 model's choice for its 4096-token
+    bucket (cached); an explicit set_tune_config switches it off, set_auto_tune(True) back on."""
+    m = moe()
+    from paper_2604_19241_b200.model import choose_config
+    H, F, E, k = 2048, 768, 128, 8
+    L = m.EpMoE(H, F, E, k, 16384)
+    for T in (300, 16384):
+        ids = torch.randint(0, E, (T, 1), device="cuda").int().repeat(1, k)
+        ids = (ids + torch.arange(k, device="cuda").int()) % E  # distinct experts per token
+        gw = torch.full((T, k), 1.0 / k, device="cuda")
+        L.plan(ids, gw)
+        got = L.tune_config()
+        want = choose_config(H, F, E, k, ((T + 4095) // 4096) * 4096, 1)
+        assert (got.n_disp, got.n_relay, got.n_red) == (want.n_disp, want.n_relay, want.n_red), (T, got, want)
+    L.set_tune_config((40, 0, 1, 148, 8))
+    L.plan(ids, gw)
+    assert L.tune_config().n_disp == 40
+    L.set_auto_tune(True)
+    L.plan(ids, gw)
+    assert L.tune_config().n_disp == want.n_disp
+    L.close()

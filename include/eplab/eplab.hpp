@@ -19,6 +19,9 @@
 #include <string>
 #include <vector>
 
+// The eplab:: API is exported from libeplab_b200.so (built with -fvisibility=hidden) so that
+// reference-style C++ callers link against it directly.
+#pragma GCC visibility push(default)
 namespace eplab {
 
 class ValidationError : public std::runtime_error {
@@ -226,3 +229,4 @@ class TuneCache {
 };
 
 }  // namespace eplab
+#pragma GCC visibility pop

@@ -137,3 +137,30 @@ def test_b200_layer_model_sanity():
     assert a2a.total > 0 and ag.total > 0
     best, lmin, ev = m.search_layer(q, m.hw(8))
     assert best.n_disp + best.n_relay < 148 and ev > 100 and lmin > 0
+
+
+def test_cpp_caller_links_against_the_library(tmp_path):
+    """A reference-style C++ caller (tests/cpp/cpp_caller.cpp) compiles against
+    include/eplab/eplab.hpp and links libeplab_b200.so (the eplab:: API is exported); its results
+    equal the C-ABI's, the oracle's, and the model's choice (host-only calls, no GPU)."""
+    import json, os, subprocess
+    import numpy as np
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_2604_19241_b200")
+    exe = str(tmp_path / "cpp_caller")
+    subprocess.check_call(["g++", "-std=c++20", "-O1", "-I", os.path.join(root, "include"),
+                           os.path.join(root, "tests", "cpp", "cpp_caller.cpp"), "-L", libdir,
+                           "-leplab_b200", "-Wl,-rpath," + libdir, "-o", exe])
+    out = json.loads(subprocess.check_output([exe], text=True).strip())
+    from oracle import pyoracle as po
+    from paper_2604_19241_b200.model import choose_config, sample_routing
+    sel, gw = sample_routing(128, 8, 1024, 8, 7)
+    osel, ogw = po.Oracle().sample_routing(128, 8, 1024, 8, 7)
+    assert out["sel0"] == sel[0, 0] == osel[0, 0]
+    assert np.float32(out["gw0"]) == gw[0, 0] == ogw[0, 0]
+    _, _, off, _, _ = po.Oracle().token_map(osel, 128, 8)
+    assert out["off_sum"] == int(off.sum())
+    want = choose_config(2048, 768, 128, 8, 16384, 8)
+    best_n_disp = out["n_disp"]  # raw search_layer result (choose_config applies the comm-CTA floor)
+    assert out["n_relay"] == want.n_relay and best_n_disp <= want.n_disp
+    assert out["validation_error"] is True

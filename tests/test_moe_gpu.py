@@ -442,3 +442,39 @@ def test_auto_tune_per_token_bucket():
     L.plan(ids, gw)
     assert L.tune_config().n_disp == want.n_disp
     L.close()
+
+
+def test_cpp_device_api_layer_matches_oracle(tmp_path):
+    """The C++ data-path twins of the reference operators (include/eplab/device.hpp:
+    build_global_token_map, dispatch_group_gemm, group_gemm_combine, *_bwd) called from a compiled
+    C++ program match the oracle, repeat bitwise, and throw the reference's ValidationError."""
+    import json, subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_2604_19241_b200")
+    exe, out = str(tmp_path / "cpp_layer"), str(tmp_path / "layer.bin")
+    subprocess.check_call(["g++", "-std=c++20", "-O1", "-I", os.path.join(root, "include"), "-I",
+                           "/usr/local/cuda/include", os.path.join(root, "tests", "cpp", "cpp_layer.cpp"),
+                           "-L", libdir, "-leplab_b200", "-L", "/usr/local/cuda/lib64", "-lcudart",
+                           "-Wl,-rpath," + libdir, "-Wl,-rpath,/usr/local/cuda/lib64", "-o", exe])
+    res = json.loads(subprocess.check_output([exe, out], text=True).strip().splitlines()[-1])
+    assert res == {"bitwise_repeat": True, "validation_error": True}
+    E, k, H, F, T = 8, 2, 256, 256, 192
+    raw = open(out, "rb").read()
+    pos = 0
+
+    def take(dt, n):
+        nonlocal pos
+        a = np.frombuffer(raw, dtype=dt, count=n, offset=pos)
+        pos += a.nbytes
+        return a
+
+    sel, gw = take(np.int32, T * k), take(np.float32, T * k)
+    x, dy = take(np.uint16, T * H), take(np.uint16, T * H)
+    w_up, w_down = take(np.uint16, E * 2 * F * H), take(np.uint16, E * H * F)
+    y, dx, dg = take(np.uint16, T * H), take(np.uint16, T * H), take(np.float32, T * k)
+    dwu, dwd = take(np.uint16, E * 2 * F * H), take(np.uint16, E * H * F)
+    ref = po.Oracle().moe_layer(1, E, k, H, F, sel.reshape(1, -1), gw.reshape(1, -1), x.reshape(1, T, H),
+                                w_up.reshape(E, 2 * F, H), w_down.reshape(E, H, F), dy.reshape(1, T, H))
+    for key, got in (("y", y), ("dx", dx), ("dw_up", dwu), ("dw_down", dwd)):
+        assert_close(bf16_to_f32(got), bf16_to_f32(ref[key]).reshape(-1), key)
+    assert_close(dg, ref["dgate"].reshape(-1), "dgate")

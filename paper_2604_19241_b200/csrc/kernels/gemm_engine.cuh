@@ -19,6 +19,18 @@ template <class Mode, class Args, class TL>
 __device__ __forceinline__ void call_spare(const Args& a, const TL& tl) {
   if constexpr (has_spare<Mode>::value) Mode::spare(a, tl);
 }
+// A Mode with `static constexpr bool RELEASE_AFTER = true` publishes a tile's results in
+// `Mode::epilogue_release(args, tile, row)`, called after the epilogue has handed the TMEM
+// accumulator back to the MMA issuer: the release fence (system scope at EP>1) then overlaps the
+// next tile's main loop instead of holding the accumulator.
+template <class M, class = void>
+struct has_release_after : std::false_type {};
+template <class M>
+struct has_release_after<M, std::void_t<decltype(M::RELEASE_AFTER)>> : std::bool_constant<M::RELEASE_AFTER> {};
+template <class Mode, class Args>
+__device__ __forceinline__ void call_release_after(const Args& a, const TileDesc& td, int r) {
+  if constexpr (has_release_after<Mode>::value) Mode::epilogue_release(a, td, r);
+}
 
 __device__ __forceinline__ void timeline_push(const Timeline& tl, unsigned long long t0,
                                               unsigned long long t1, uint32_t role, int task) {
@@ -167,6 +179,7 @@ __device__ int gemm_roles(const typename Mode::Args& args, const TmaSet& tm, uin
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&S->tempty[acc]);
+      call_release_after<Mode>(args, td, r);
       if (Mode::HAS_TILE_DONE || tl.rec) {
         epi_bar();  // all four epilogue warps finished this tile's stores
         if (warp == 4 && lane == 0) {

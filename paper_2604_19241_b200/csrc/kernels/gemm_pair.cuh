@@ -219,6 +219,7 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
+      if (work) call_release_after<Mode>(args, half, r);
       if (Mode::HAS_TILE_DONE || tl.rec) {
         epi_bar();
         if (warp == 4 && lane == 0) {

@@ -948,15 +948,19 @@ __device__ __forceinline__ void push_rows(const MkArgs& a, const TileDesc& td, u
     acc_chunk(taddr, c, v);
     if (live) store_row_bf16_32(dst + c * 32, v);
   }
-  if (live) {
-    uint32_t* ctr = tok_counter(S, a.d, ph, PAR(a), mt.rep / a.d.topk);
-    if (a.dbg & 256)
-      red_relaxed_sys_add(ctr, 1u);  // experiment only: no release ordering (measures the fence)
-    else if (a.d.world == 1)
-      red_release_gpu_add(ctr, 1u);  // one GPU: the reducer is on this device
-    else
-      red_release_sys_add(ctr, 1u);
-  }
+}
+
+// The combine push's scoreboard update (RELEASE_AFTER hook, after the accumulator went back to
+// the MMA issuer): this thread's replica row of the tile is counted on its source token.
+__device__ __forceinline__ void push_release(const MkArgs& a, const TileDesc& td, int r, int ph) {
+  const bool live = r < td.rows;
+  if (a.d.world == 1)
+    fence_acq_rel_gpu();  // one GPU: the reducer is on this device
+  else
+    fence_acq_rel_sys();
+  if (!live) return;
+  const SlotMeta mt = a.peers.p[a.d.rank].meta[td.m0 + r];
+  red_relaxed_sys_add(tok_counter(a.peers.p[mt.src], a.d, ph, PAR(a), mt.rep / a.d.topk), 1u);
 }
 
 // Pull this row's slot metadata (return address / gate weight) into L1 before the accumulator
@@ -970,6 +974,8 @@ __device__ __forceinline__ void prefetch_meta_l1(const MkArgs& a, const TileDesc
 struct ModeDown {
   using Args = MkArgs;
   static constexpr bool HAS_TILE_DONE = false;
+  static constexpr bool RELEASE_AFTER = true;
+  __device__ static void epilogue_release(const Args& a, const TileDesc& td, int r) { push_release(a, td, r, 0); }
   __device__ static void epilogue_prefetch(const Args& a, const TileDesc& td, int r) { prefetch_meta_l1(a, td, r); }
   __device__ static TileDesc tile_pair(const Args& a, int t) {
     return nt_tile_pair(a.d, a.p, t, a.d.H / BN, BN, a.d.F / BK, a.rgp);
@@ -1237,6 +1243,10 @@ struct ModeDgradDown {
 struct ModeDgradUp {
   using Args = MkArgs;
   static constexpr bool HAS_TILE_DONE = false;
+  static constexpr bool RELEASE_AFTER = true;
+  __device__ static void epilogue_release(const Args& a, const TileDesc& td, int r) {
+    if (!td.pad1) push_release(a, td, r, 1);  // dgrad tiles push dX replicas; wgrad tiles do not
+  }
   static constexpr bool SPARE = true;
   __device__ static void spare(const Args& a, const Timeline& tl) { spare_reduce(a, tl, 1); }
   __device__ static void epilogue_prefetch(const Args& a, const TileDesc& td, int r) { prefetch_meta_l1(a, td, r); }

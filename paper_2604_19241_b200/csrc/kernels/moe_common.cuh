@@ -134,8 +134,7 @@ struct MkArgs {
   Timeline tl;
   int dbg;  // debug bits (experiments only, results wrong): 2/4 = skip dgrad epilogue TMA stores /
             // staging, 16 = skip the saved g, u loads of the dgrad epilogue, 64 = no reduce,
-            // 128 = per-rowgroup relay timeline, 256 = combine-push counters without release
-            // ordering (the fence costs ~0.5% at EP=1 with gpu scope)
+            // 128 = per-rowgroup relay timeline
   int pair;  // 1: CTA-pair (cta_group::2) engine
   int* comm_cursor;  // [2] u64 round counter of the comm pool (zeroed per launch with cursor)
   unsigned* red_cursor;    // reduce chunk counter (zeroed per launch with cursor)

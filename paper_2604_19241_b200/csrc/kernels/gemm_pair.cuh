@@ -156,9 +156,15 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
     if (leader && lane == 0) {
       const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
       uint32_t stage = 0, phase = 0;
+      // stall accounting of the MMA issuer (timeline on): waiting for a tile (scheduler /
+      // scoreboard), for a free accumulator (epilogue), for operands (producer)
+      const bool acct = tl.rec != nullptr;
+      unsigned long long w_tile = 0, w_acc = 0, w_ops = 0, t_begin = acct ? globaltimer() : 0, tw = 0;
       for (int it = 0;; ++it) {
         const int slot = it % RING;
+        if (acct) tw = globaltimer();
         mbar_wait_cluster_wd(&S->rfull[slot], (it / RING) & 1, wd, 43);
+        if (acct) w_tile += globaltimer() - tw;
         const int t = S->ring[slot];
         const TileDesc td = S->ring_td[slot];
         mbar_arrive(&S->rempty[slot]);
@@ -166,11 +172,15 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
         const int amn = Mode::a_mn(td), bmn = Mode::b_mn(td);
         const uint32_t idesc = make_idesc(2 * BM, BN, amn, bmn);
         const uint32_t acc = it & 1;
+        if (acct) tw = globaltimer();
         mbar_wait_cluster_wd(&S->tempty[acc], ((it >> 1) & 1) ^ 1, wd, 44);
+        if (acct) w_acc += globaltimer() - tw;
         tc_fence_after();
         const uint32_t d = S->tmem_base + acc * BN;
         for (int kb = 0; kb < td.nkb; ++kb) {
+          if (acct) tw = globaltimer();
           mbar_wait_wd(&S->full[stage], phase, wd, 45);
+          if (acct) w_ops += globaltimer() - tw;
           tc_fence_after();
           const uint32_t as = a0 + stage * P_HALF_BYTES;
           const uint32_t bs = b0 + stage * P_HALF_BYTES;
@@ -189,6 +199,11 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
           }
         }
         umma_commit_pair(&S->tfull[acc]);
+      }
+      if (acct) {  // three records per CTA pair, durations = the stall totals (task -9001..-9003)
+        timeline_push(tl, t_begin, t_begin + w_tile, ROLE_COMP, -9001);
+        timeline_push(tl, t_begin, t_begin + w_acc, ROLE_COMP, -9002);
+        timeline_push(tl, t_begin, t_begin + w_ops, ROLE_COMP, -9003);
       }
     }
   } else if (warp >= 4) {

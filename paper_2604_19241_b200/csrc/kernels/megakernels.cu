@@ -935,19 +935,48 @@ struct ModeUp {
 
 // Push the 128x256 output tile row by row into the source's replica slots (over NVLink when
 // the source is a peer) and count the column tile on the source token (combine scoreboard).
+// The warp's 32 rows x 64 columns (two accumulator chunks) go through its staging area
+// (32 rows x 128 B, 16-byte granules XOR-swizzled by row) so that every store instruction writes
+// four whole 128-byte row segments -- full lines to the (possibly remote, over NVLink) replica
+// slots instead of 32 scattered 16-byte pieces.
 __device__ __forceinline__ void push_rows(const MkArgs& a, const TileDesc& td, uint32_t taddr,
-                                          int r, int ph) {
+                                          int r, int ph, uint8_t* stg) {
+  const int lane = r & 31;
   const bool live = r < td.rows;
   SlotMeta mt{0, 0, 0.f, 0};
   if (live) mt = a.peers.p[a.d.rank].meta[td.m0 + r];
   const SymPtrs& S = a.peers.p[live ? mt.src : 0];
   __nv_bfloat16* dst = (ph == 0 ? S.rep : S.rep_dx) + (size_t)mt.rep * a.d.H + td.n0;
+  const unsigned live_mask = __ballot_sync(0xffffffffu, live);
 #pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
-    float v[32];
-    acc_chunk(taddr, c, v);
-    if (live) store_row_bf16_32(dst + c * 32, v);
+  for (int c = 0; c < BN / 32; c += 2) {
+    float v0[32], v1[32];
+    acc_chunk(taddr, c, v0);
+    acc_chunk(taddr, c + 1, v1);
+    __syncwarp();  // the previous pair's reads of the staging area are done
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      const float* v = g < 4 ? v0 : v1;
+      const int o = (g & 3) * 8;
+      const int4 w = make_int4((int)pack_bf16(v[o], v[o + 1]), (int)pack_bf16(v[o + 2], v[o + 3]),
+                               (int)pack_bf16(v[o + 4], v[o + 5]), (int)pack_bf16(v[o + 6], v[o + 7]));
+      *reinterpret_cast<int4*>(stg + lane * 128 + ((g ^ (lane & 7)) << 4)) = w;
+    }
+    __syncwarp();
+    // 4 rows per instruction, 8 lanes x 16 B per row
+    const int sub = lane >> 3, gran = lane & 7;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int row = i * 4 + sub;
+      const unsigned long long dp =
+          __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst), row);
+      if ((live_mask >> row) & 1u) {
+        const int4 w = *reinterpret_cast<const int4*>(stg + row * 128 + ((gran ^ (row & 7)) << 4));
+        reinterpret_cast<int4*>(reinterpret_cast<__nv_bfloat16*>(dp) + c * 32)[gran] = w;
+      }
+    }
   }
+  __syncwarp();  // staging free for the next tile; every row's stores precede its owner's release
 }
 
 // The combine push's scoreboard update (RELEASE_AFTER hook, after the accumulator went back to
@@ -1006,8 +1035,8 @@ struct ModeDown {
     tma_load_2d(&tm.m[1], bar, s, kb * BK, td.e * a.d.H + td.n0);
   }
   __device__ static void epilogue(const Args& a, const TmaSet&, const TileDesc& td, uint32_t taddr,
-                                  int r, uint8_t*) {
-    push_rows(a, td, taddr, r, 0);
+                                  int r, uint8_t* stg) {
+    push_rows(a, td, taddr, r, 0, stg);
   }
   template <class A>
   __device__ static void tile_done(const A&, const TileDesc&) {}
@@ -1310,7 +1339,7 @@ struct ModeDgradUp {
   __device__ static void epilogue(const Args& a, const TmaSet& tm, const TileDesc& td,
                                   uint32_t taddr, int r, uint8_t* stg) {
     if (!td.pad1) {
-      push_rows(a, td, taddr, r, 1);
+      push_rows(a, td, taddr, r, 1, stg);
       return;
     }
     wgrad_store(&tm.m[6], td, 2 * a.d.F, taddr, r, stg);

@@ -537,6 +537,11 @@ int eplab_dispatch_group_gemm_bwd(eplab_ctx* c, const void* dy, const void* w_do
     cudaStream_t st = (cudaStream_t)stream;
     CK(cudaMemsetAsync(c->wg_cnt, 0, (size_t)c->d.epr * (c->d.F / 256) * 4, st));
     MkArgs a = base_args(c);
+    // the backward dispatch moves twice the bytes of the forward one (dY rows plus the o rows
+    // of the gate gradient): twice the comm CTAs, within the deadlock constraint
+    // (profiles/r01_ndisp_sweep_bwd.txt)
+    const int scale = getenv("EPLAB_BWD_DISP_SCALE") ? std::max(1, atoi(getenv("EPLAB_BWD_DISP_SCALE"))) : 2;
+    a.n_disp = std::max(a.n_disp, std::min(a.n_disp * scale, c->num_sms / 2 - a.n_relay));
     a.dy = static_cast<const __nv_bfloat16*>(dy);
     a.w_down = static_cast<const __nv_bfloat16*>(w_down);
     a.dw_down = static_cast<__nv_bfloat16*>(dw_down);

@@ -14,6 +14,7 @@ ap.add_argument("--config", default="mixtral")
 ap.add_argument("--ncu", action="store_true")
 ap.add_argument("--out", default="gpurun_out")
 ap.add_argument("--cfg", default="")
+ap.add_argument("--sms", type=int, default=0, help="persistent-grid SM budget (0: all)")
 args = ap.parse_args()
 H, F, E, k, T = bench.CONFIGS[args.config]
 sel, gw = po.Oracle().sample_routing(E, k, T, 1, 7)
@@ -23,7 +24,9 @@ x = torch.randn(T, H, device="cuda", generator=g).bfloat16(); dy = (torch.randn(
 w_up = (torch.randn(E, 2 * F, H, device="cuda", generator=g) * H ** -0.5).bfloat16()
 w_down = (torch.randn(E, H, F, device="cuda", generator=g) * F ** -0.5).bfloat16()
 L = M.EpMoE(H, F, E, k, T)
-cfg = choose_config(H, F, E, k, T, 1) if not args.cfg else M.TuneConfig(*[int(v) for v in args.cfg.split(",")])
+if args.sms:
+    L.set_sm_budget(args.sms)
+cfg = choose_config(H, F, E, k, T, 1, n_sm=args.sms or 148) if not args.cfg else M.TuneConfig(*[int(v) for v in args.cfg.split(",")])
 L.set_tune_config(cfg)
 y = torch.empty(T, H, device="cuda", dtype=torch.bfloat16)
 out = dict(dx=torch.empty(T, H, dtype=torch.bfloat16, device="cuda"), dw_up=torch.empty_like(w_up),

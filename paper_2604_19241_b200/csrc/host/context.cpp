@@ -294,6 +294,8 @@ int eplab_init(const eplab_init_args* args, eplab_ctx** out) {
     c->st_hact = eplab_host::make_store_map(c->hact, M, d.F);
     c->st_dgu = eplab_host::make_store_map(c->dgu, M, 2 * d.F);
     c->st_hw = eplab_host::make_store_map(c->hw, M, d.F);
+    if (eplab_launch::preload_megakernels() || eplab_launch::preload_plan())
+      throw Fail{EPLAB_ERR_INTERNAL, std::string("kernel preload: ") + cudaGetErrorString(cudaGetLastError())};
     CK(cudaDeviceSynchronize());
     *out = c;
   });

@@ -5,6 +5,8 @@
 #include "kernels/moe_common.cuh"
 
 namespace eplab_launch {
+int preload_megakernels();
+int preload_plan();
 int plan_launch(const eplab_dev::Dims& d, const eplab_dev::Peers& peers,
                 const eplab_dev::PlanDev& p, uint32_t* epoch, uint64_t timeout_ns, int* err,
                 cudaStream_t st);

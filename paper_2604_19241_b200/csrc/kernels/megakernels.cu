@@ -1503,28 +1503,31 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 namespace eplab_launch {
 using namespace eplab_dev;
 
+// Loads every MegaKernel into the current device's context and sets its shared-memory size --
+// called by eplab_init on each context's device. With CUDA's lazy module loading the first
+// launch of a function can wait for the device to idle, which never happens while another
+// virtual rank's kernel spins on a scoreboard fed by a kernel this host thread has yet to launch.
+int preload_megakernels() {
+  auto set = [](auto fn) {
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM_BYTES) ==
+           cudaSuccess;
+  };
+  const bool ok = set(megakernel<0, ModeUp>) && set(megakernel<1, ModeDown>) &&
+                  set(megakernel<2, ModeDgradDown>) && set(megakernel<3, ModeDgradUp>) &&
+                  set(megakernel_pair<0, ModeUp>) && set(megakernel_pair<1, ModeDown>) &&
+                  set(megakernel_pair<2, ModeDgradDown>) && set(megakernel_pair<3, ModeDgradUp>);
+  return ok ? 0 : 1;
+}
+
 template <int KIND, class Mode>
 static int launch_mk(const TmaSet& tm, const MkArgs& a, int grid, cudaStream_t st) {
-  static bool attr = false, attr_p = false;
   cudaMemsetAsync(a.cursor, 0, 32, st);  // task cursor, comm rounds, reduce chunks, relay rowgroups
   if (!a.pair) {
     auto fn = megakernel<KIND, Mode>;
-    if (!attr) {
-      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)GEMM_SMEM_BYTES) != cudaSuccess)
-        return 1;
-      attr = true;
-    }
     fn<<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, st>>>(tm, a);
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
   }
   auto fn = megakernel_pair<KIND, Mode>;
-  if (!attr_p) {
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)GEMM_SMEM_BYTES) != cudaSuccess)
-      return 1;
-    attr_p = true;
-  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((grid / 2) * 2);
   cfg.blockDim = dim3(GEMM_THREADS);

@@ -212,6 +212,17 @@ int plan_launch(const Dims& d, const Peers& peers, const PlanDev& p, uint32_t* e
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
+// Loads the planning kernels into the current context up front (see preload_megakernels): the
+// count exchange of plan_global_kernel spins until every virtual rank's planner has run.
+int preload_plan() {
+  cudaFuncAttributes fa;
+  const bool ok = cudaFuncGetAttributes(&fa, plan_hist_kernel) == cudaSuccess &&
+                  cudaFuncGetAttributes(&fa, plan_global_kernel) == cudaSuccess &&
+                  cudaFuncGetAttributes(&fa, plan_entries_kernel) == cudaSuccess &&
+                  cudaFuncGetAttributes(&fa, zero_padding_kernel) == cudaSuccess;
+  return ok ? 0 : 1;
+}
+
 int zero_padding_launch(const Dims& d, const PlanDev& p, __nv_bfloat16* recv, cudaStream_t st) {
   dim3 grid(4, d.epr);
   zero_padding_kernel<<<grid, 256, 0, st>>>(d, p, recv);

@@ -478,3 +478,16 @@ def test_cpp_device_api_layer_matches_oracle(tmp_path):
     for key, got in (("y", y), ("dx", dx), ("dw_up", dwu), ("dw_down", dwd)):
         assert_close(bf16_to_f32(got), bf16_to_f32(ref[key]).reshape(-1), key)
     assert_close(dg, ref["dgate"].reshape(-1), "dgate")
+
+
+def test_allgather_regime_ep4_top8_relay_equals_alltoall():
+    """DeepSeek-style AllGather regime (top-8 of 32 experts on 4 virtual ranks: most tokens have
+    several experts per rank): relay on (dedup + relay pool) and relay off give identical results,
+    and both match the oracle."""
+    prob = Problem(4, 32, 8, 256, 256, 96, seed=21)
+    rel, _, _ = run_layer(prob, cfg=(2, 2, 1, 37, 8))
+    a2a, _, _ = run_layer(prob, cfg=(4, 0, 1, 37, 8))
+    gr, ga = gather(rel[0]), gather(a2a[0])
+    for key in ("y", "dx", "dgate", "dw_up", "dw_down"):
+        assert (gr[key] == ga[key]).all(), key
+    check_vs_oracle(prob, gr)

@@ -461,7 +461,7 @@ def run_ours(args):
         t_nvl = nvl_tok * T / (NVL_GBS * 1e9)
         roof_ms = max(t_gemm, t_nvl) * 1e3
         t_hbm = hbm_bytes_per_step(args.config, world) / (hbm * 1e9)
-        cpu = cpu_baseline(args.config) if not args.no_cpu_baseline else None
+        cpu = cpu_baseline(args.config) if (world == 1 and not args.no_cpu_baseline) else None  # N=1 only
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",

@@ -155,6 +155,7 @@ MkArgs base_args(eplab_ctx* c) {
   if (const char* e = getenv("EPLAB_SPARE")) a.spare_warps = atoi(e);
   a.rgp = getenv("EPLAB_RGP") ? std::max(1, atoi(getenv("EPLAB_RGP"))) : 8;
   a.tngp = getenv("EPLAB_TNGP") ? std::max(1, atoi(getenv("EPLAB_TNGP"))) : 4;
+  a.tngp_d = getenv("EPLAB_TNGP_D") ? std::max(1, atoi(getenv("EPLAB_TNGP_D"))) : 4;  // profiles/r01_wgrad_raster.txt
   // somebody must move the rows: the bulk mover and spare-less pools need >= 1 comm CTA
   if (a.n_disp == 0 && (a.comm_bulk || !(a.spare_warps & 1))) a.n_disp = 1;
   return a;

@@ -1084,7 +1084,7 @@ struct ModeDgradDown {
   __device__ static TileDesc tile_pair(const Args& a, int t) {
     const int nd = n_dgrad_pair(a);
     if (t < nd) return nt_tile_pair(a.d, a.p, t, a.d.F / BN, BN, a.d.H / BK, a.rgp);
-    return tn_tile_pair(a.d, a.p, t - nd, a.d.H, a.d.F, a.tngp);
+    return tn_tile_pair(a.d, a.p, t - nd, a.d.H, a.d.F, a.tngp_d);
   }
   __device__ static void before_loads_pair(const Args& a, const TileDesc& td) {
     if (!td.pad1)

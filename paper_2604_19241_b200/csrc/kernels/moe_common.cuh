@@ -142,7 +142,8 @@ struct MkArgs {
   int spare_warps;  // bit 0: the GEMM CTAs' spare warps join the comm pool (warp split),
                     // bit 1: ... and the backward combine's reduce pool
   int comm_bulk;
-  int rgp, tngp;  // CTA-pair raster groups: 256-row blocks per NT group, 256-row output blocks per TN group  // 1: comm role moves rows with the TMA bulk-copy engine (EPLAB_COMM=bulk)
+  int rgp, tngp, tngp_d;  // CTA-pair raster groups: 256-row blocks per NT group, 256-row output
+                          // blocks per TN group (up weight gradient / down weight gradient)  // 1: comm role moves rows with the TMA bulk-copy engine (EPLAB_COMM=bulk)
 };
 
 }  // namespace eplab_dev

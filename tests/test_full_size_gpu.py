@@ -127,3 +127,62 @@ def test_world_invariance_full_size_qwen3_ep8(relay):
     assert torch.equal(torch.cat([gg["dw_down"] for gg in gs]), g1["dw_down"]), "dw_down"
     for r in ranks:
         r.close()
+
+
+def test_small_config_ep2_full_size():
+    """BASELINE configs[0] at its stated size (8 experts top-2, H 1024, F 2048, 4096 tokens per rank,
+    EP=2 on two virtual ranks): equal to EP=1 on the same 8192 tokens bit for bit, and sampled tokens'
+    y / dx / dgate equal the oracle run on those tokens alone."""
+    from paper_2604_19241_b200 import moe as M
+    from paper_2604_19241_b200.model import sample_routing
+    H, F, E, k, T, W = 1024, 2048, 8, 2, 4096, 2
+    sel, gw = sample_routing(E, k, T, W, 7)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(W * T, H, device="cuda", generator=g).bfloat16()
+    dy = (torch.randn(W * T, H, device="cuda", generator=g) * 0.5).bfloat16()
+    w_up = (torch.randn(E, 2 * F, H, device="cuda", generator=g) * H ** -0.5).bfloat16()
+    w_down = (torch.randn(E, H, F, device="cuda", generator=g) * F ** -0.5).bfloat16()
+    ids = torch.from_numpy(sel.reshape(W * T, k).copy()).cuda()
+    gws = torch.from_numpy(gw.reshape(W * T, k).copy()).cuda()
+    one = M.EpMoE(H, F, E, k, W * T)
+    y1 = one.forward(x, ids, gws, w_up, w_down)
+    g1 = one.backward(dy, w_up, w_down)
+    one.check()
+    torch.cuda.synchronize()
+    one.close()
+    epr = E // W
+    ranks = [M.EpMoE(H, F, E, k, T, rank=r, world=W, timeout_s=60.0) for r in range(W)]
+    M.EpMoE.connect_local(ranks)
+    for r in ranks:
+        r.set_sm_budget(148 // W)
+    streams = [torch.cuda.Stream() for _ in range(W)]
+    ys, gs = [None] * W, [None] * W
+    for ph in range(3):
+        for r in range(W):
+            sl = slice(r * T, (r + 1) * T)
+            with torch.cuda.stream(streams[r]):
+                if ph == 0:
+                    ranks[r].plan(ids[sl], gws[sl], streams[r])
+                elif ph == 1:
+                    ranks[r].dispatch_group_gemm(x[sl], w_up[r * epr:(r + 1) * epr], streams[r])
+                    ys[r] = ranks[r].group_gemm_combine(w_down[r * epr:(r + 1) * epr], stream=streams[r])
+                else:
+                    gs[r] = ranks[r].backward(dy[sl], w_up[r * epr:(r + 1) * epr], w_down[r * epr:(r + 1) * epr],
+                                              stream=streams[r])
+        if ph == 0:
+            torch.cuda.synchronize()
+    for r in range(W):
+        ranks[r].check(streams[r])
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(ys), y1)
+    for key in ("dx", "dgate", "dw_up", "dw_down"):
+        assert torch.equal(torch.cat([gg[key] for gg in gs]), g1[key]), key
+    toks = np.array([0, 5, T - 1, T, W * T - 1])
+    ref = po.Oracle().moe_layer(1, E, k, H, F, sel.reshape(W * T, k)[toks].reshape(1, -1),
+                                gw.reshape(W * T, k)[toks].reshape(1, -1), to_u16(x[toks]).reshape(1, -1, H),
+                                to_u16(w_up), to_u16(w_down), to_u16(dy[toks]).reshape(1, -1, H))
+    assert_close(bf16_to_f32(to_u16(y1[toks])).reshape(-1), bf16_to_f32(ref["y"]).reshape(-1), "y")
+    assert_close(bf16_to_f32(to_u16(g1["dx"][toks])).reshape(-1), bf16_to_f32(ref["dx"]).reshape(-1), "dx")
+    assert_close(g1["dgate"][toks].cpu().numpy().reshape(-1), ref["dgate"].reshape(-1), "dgate")
+    for r in ranks:
+        r.close()

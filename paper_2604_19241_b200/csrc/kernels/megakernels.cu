@@ -1190,9 +1190,7 @@ struct ModeDgradDown {
     }
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
-      float v[32];
-      acc_chunk(taddr, c, v);
-      int4 gn[4], un[4];
+      int4 gn[4], un[4];  // issued before this chunk's TMEM load so they also overlap its wait
       if (ld_gu && c + 1 < BN / 32) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -1200,6 +1198,8 @@ struct ModeDgradDown {
           un[i] = usrc[(c + 1) * 4 + i];
         }
       }
+      float v[32];
+      acc_chunk(taddr, c, v);
       uint32_t pdg[16], pdu[16], phw[16];
       if (live) {
 #pragma unroll

@@ -6,15 +6,20 @@
 //   routing.hpp:15       sample_routing
 //   token_map.hpp:22-93  local_stable_sort, compute_global_offsets, build_global_token_map,
 //                        build_send_schedule
-//   traffic.hpp:28-51    distinct_rank_distribution, volume_expected, volume_exact
+//   traffic.hpp:14-51    BigInt, stirling2, distinct_rank_distribution, volume_expected, volume_exact
+//   precision.hpp:16-52  OrderPolicy, ReductionTerm, ReductionPlan, accumulate, PrecisionReport,
+//                        fused_vs_sequential, split_batch_experiment
+//   softfloat.hpp:10-28  FpFormat, round_to_bf16, fp_round, fp_add, fp_mul, bit_equal
 //   perf_model.hpp:38-62 effective_bandwidth ... predict_latency (reference-compatible)
 //   tuner.hpp:16-82      enumerate_space, search, TuneCache
 // B200 additions: b200_hardware(), predict_layer() (fwd+bwd model of the MegaKernels built
 // here, incl. the relay-off AllToAll mode), search_layer().
 #pragma once
+#include <algorithm>
 #include <cstdint>
 #include <functional>
 #include <map>
+#include <cstdio>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -73,6 +78,8 @@ struct RoutingInstance {
 HardwareSpec validate_hardware(HardwareSpec spec);
 std::pair<MoEShape, HardwareSpec> validate_shape(MoEShape shape, HardwareSpec spec);
 void validate_tune_config(const TuneConfig& cfg, const HardwareSpec& spec);
+// Post-dispatch token count per rank under balanced routing (types.hpp:79).
+long long derive_expanded_tokens(const MoEShape& shape, int world);
 void validate_routing(const RoutingInstance& routing);
 
 RoutingInstance sample_routing(const MoEShape& shape, int world, std::uint64_t seed);
@@ -103,6 +110,10 @@ struct GlobalTokenMap {
   std::vector<MapEntry> entries;
   std::vector<long long> recv_totals, recv_segment_base;
   const MapEntry& at(long long t, int j) const { return entries[t * topk + j]; }
+  long long recv_total(int rank_, int e_loc) const { return recv_totals[(size_t)rank_ * experts_per_rank + e_loc]; }
+  long long segment_base(int rank_, int e_loc) const {
+    return recv_segment_base[(size_t)rank_ * experts_per_rank + e_loc];
+  }
 };
 std::vector<GlobalTokenMap> build_global_token_map(const RoutingInstance& routing);
 struct SendItem {
@@ -116,12 +127,122 @@ struct SendSchedule {
   std::vector<SendItem> items;
 };
 SendSchedule build_send_schedule(const GlobalTokenMap& map);
+// One row per (rank, t, j) plus a header, for diffing against oracles (token_map.hpp:91).
+std::string export_map_table(const std::vector<GlobalTokenMap>& maps);
 
 // --------------------------------------------------------------- traffic
+// Exact non-negative integers of any size (the role of boost::multiprecision::cpp_int in
+// traffic.hpp:6-10): base-2^32 limbs, the operations the exact traffic arithmetic needs.
+class BigInt {
+ public:
+  BigInt(unsigned long long v = 0) { set(v); }  // NOLINT: implicit, like cpp_int
+  BigInt(long long v) { set(v < 0 ? 0ULL : (unsigned long long)v); }
+  BigInt(int v) { set(v < 0 ? 0ULL : (unsigned long long)v); }
+  BigInt(unsigned __int128 v) {
+    while (v) {
+      l_.push_back((uint32_t)v);
+      v >>= 32;
+    }
+  }
+  explicit BigInt(const char* dec) {
+    for (const char* c = dec; *c; ++c) {
+      if (*c < '0' || *c > '9') throw std::invalid_argument("BigInt: not a decimal number");
+      *this = *this * BigInt(10) + BigInt(*c - '0');
+    }
+  }
+  BigInt& operator+=(const BigInt& o) {
+    uint64_t carry = 0;
+    if (l_.size() < o.l_.size()) l_.resize(o.l_.size(), 0);
+    for (size_t i = 0; i < l_.size(); ++i) {
+      const uint64_t s = (uint64_t)l_[i] + (i < o.l_.size() ? o.l_[i] : 0) + carry;
+      l_[i] = (uint32_t)s;
+      carry = s >> 32;
+    }
+    if (carry) l_.push_back((uint32_t)carry);
+    return *this;
+  }
+  friend BigInt operator+(BigInt a, const BigInt& b) { return a += b; }
+  friend BigInt operator*(const BigInt& a, const BigInt& b) {
+    BigInt r;
+    if (a.l_.empty() || b.l_.empty()) return r;
+    std::vector<uint64_t> acc(a.l_.size() + b.l_.size() + 1, 0);
+    for (size_t i = 0; i < a.l_.size(); ++i) {
+      uint64_t carry = 0;
+      for (size_t j = 0; j < b.l_.size(); ++j) {
+        const uint64_t cur = acc[i + j] + (uint64_t)a.l_[i] * b.l_[j] + carry;
+        acc[i + j] = cur & 0xFFFFFFFFull;
+        carry = cur >> 32;
+      }
+      for (size_t k = i + b.l_.size(); carry; ++k) {
+        const uint64_t cur = acc[k] + carry;
+        acc[k] = cur & 0xFFFFFFFFull;
+        carry = cur >> 32;
+      }
+    }
+    r.l_.assign(acc.begin(), acc.end());
+    r.trim();
+    return r;
+  }
+  BigInt& operator*=(const BigInt& o) { return *this = *this * o; }
+  friend bool operator==(const BigInt& a, const BigInt& b) { return a.l_ == b.l_; }
+  friend bool operator!=(const BigInt& a, const BigInt& b) { return !(a == b); }
+  friend bool operator<(const BigInt& a, const BigInt& b) {
+    if (a.l_.size() != b.l_.size()) return a.l_.size() < b.l_.size();
+    for (size_t i = a.l_.size(); i-- > 0;)
+      if (a.l_[i] != b.l_[i]) return a.l_[i] < b.l_[i];
+    return false;
+  }
+  friend bool operator>(const BigInt& a, const BigInt& b) { return b < a; }
+  friend bool operator<=(const BigInt& a, const BigInt& b) { return !(b < a); }
+  friend bool operator>=(const BigInt& a, const BigInt& b) { return !(a < b); }
+  double to_double() const {
+    double r = 0;
+    for (size_t i = l_.size(); i-- > 0;) r = r * 4294967296.0 + l_[i];
+    return r;
+  }
+  template <class T>
+  T convert_to() const {
+    return (T)to_double();
+  }
+  std::string str() const {
+    if (l_.empty()) return "0";
+    std::vector<uint32_t> v = l_;
+    std::string out;
+    while (!v.empty()) {  // repeated division by 10^9
+      uint64_t rem = 0;
+      for (size_t i = v.size(); i-- > 0;) {
+        const uint64_t cur = (rem << 32) | v[i];
+        v[i] = (uint32_t)(cur / 1000000000u);
+        rem = cur % 1000000000u;
+      }
+      while (!v.empty() && v.back() == 0) v.pop_back();
+      char buf[16];
+      std::snprintf(buf, sizeof buf, v.empty() ? "%llu" : "%09llu", (unsigned long long)rem);
+      out.insert(0, buf);
+    }
+    return out;
+  }
+
+ private:
+  void set(unsigned long long v) {
+    l_.clear();
+    while (v) {
+      l_.push_back((uint32_t)v);
+      v >>= 32;
+    }
+  }
+  void trim() {
+    while (!l_.empty() && l_.back() == 0) l_.pop_back();
+  }
+  std::vector<uint32_t> l_;  // little-endian base-2^32 limbs, no leading zeros
+};
+
+// Stirling numbers of the second kind, exact, 0 <= k <= n <= 64 (traffic.hpp:16).
+BigInt stirling2(int n, int k);
 struct DistinctRankDistribution {
   int world = 0, topk = 0;
-  std::vector<unsigned __int128> numerators;  // index x-1
-  unsigned __int128 denominator = 1;
+  std::vector<BigInt> numerators;  // index x-1, x in [1, min(topk, world)]
+  BigInt denominator = 1;          // world^topk
   std::vector<double> probs;
   double expectation = 0, expected_saving_fraction = 0;
   double prob(int x) const { return probs[x - 1]; }
@@ -130,6 +251,7 @@ DistinctRankDistribution distinct_rank_distribution(int world, int topk);
 enum class SelfRankAccounting { IncludeSelf, RemoteOnly };
 struct TrafficReport {
   double v_allgather = 0, v_alltoall = 0, v_megakernel_nvl = 0, v_megakernel_hbm = 0;
+  enum class Basis { Expected, ExactInstance } basis = Basis::Expected;  // traffic.hpp:44
 };
 TrafficReport volume_expected(const MoEShape& shape, const HardwareSpec& spec,
                               SelfRankAccounting acc = SelfRankAccounting::IncludeSelf);
@@ -139,6 +261,50 @@ TrafficReport volume_exact(const RoutingInstance& routing, const MoEShape& shape
 // Exact E[#distinct remote ranks] for top-k drawn WITHOUT replacement from n_exp experts
 // spread evenly over `world` ranks.
 double expected_remote_ranks(int n_exp, int world, int topk);
+
+// --------------------------------------------------------------- softfloat / precision
+// softfloat.hpp:10-28: round-to-nearest-even to bfloat16 carried in binary32; fp_add / fp_mul round
+// their binary32 result to the format (an accumulate-then-round pipeline).
+enum class FpFormat { Binary32, Bfloat16 };
+float round_to_bf16(float x);
+float fp_round(float x, FpFormat fmt);
+float fp_add(float a, float b, FpFormat fmt);
+float fp_mul(float a, float b, FpFormat fmt);
+bool bit_equal(float a, float b);
+
+// precision.hpp:16-52. The k-ordered combine: a token's replicas folded in plan order, every
+// intermediate rounded to the format. With FpFormat::Binary32 this is, bit for bit, the fold of
+// the MegaKernels' reduce role (y = round_to_bf16(accumulate(plan, Binary32)), tests/test_parity_gpu.py).
+enum class OrderPolicy { Canonical, Permuted, SplitBatch };
+struct ReductionTerm {
+  int k = 0;
+  float weight = 0;
+  float value = 0;
+};
+struct ReductionPlan {
+  std::vector<std::vector<ReductionTerm>> tokens;
+};
+std::vector<float> accumulate(const ReductionPlan& plan, FpFormat fmt);
+struct PrecisionReport {
+  double max_diff = 0;
+  double frac_non_bitwise = 0;
+  long long elements = 0;
+  long long non_bitwise = 0;
+};
+// Path A: the sequential k-ascending fold; path B: the fused combine of this build -- a token is
+// reduced only after all top-k replicas landed (the reduce role's top-k barrier) and folded in
+// canonical slot order whatever order they arrived in (here: a seeded random arrival order per
+// token, as replicas from different expert tiles and ranks land). control = Permuted folds path B
+// in a seeded per-token permutation instead (the broken-reducer control). The reference derives
+// arrival times from its combine simulator (precision.cpp:54-96); the fold order, the contract, is
+// the same.
+PrecisionReport fused_vs_sequential(const RoutingInstance& routing, const MoEShape& shape,
+                                    const HardwareSpec& spec, const TuneConfig& cfg, std::uint64_t seed,
+                                    FpFormat fmt, OrderPolicy control = OrderPolicy::Canonical);
+// Weight-gradient style column sums: full left-fold over the token axis vs (first half) + (second
+// half) (precision.cpp:98-134). split_at < 0 means n_tok / 2.
+PrecisionReport split_batch_experiment(const MoEShape& shape, std::uint64_t seed, FpFormat fmt,
+                                       long long split_at = -1);
 
 // --------------------------------------------------------------- perf model (reference Alg. 2)
 enum class ResidualScaling { AsPrinted, Redistributed };

@@ -120,10 +120,14 @@ typedef struct {
 EPLAB_API int eplab_init(const eplab_init_args* args, eplab_ctx** out);
 EPLAB_API int eplab_destroy(eplab_ctx* ctx);
 
-/* Peer wiring. Multi-process: export my region's CUDA IPC handle (64 bytes), all-gather the
- * handles (NCCL / torch.distributed bootstrap) and import them (world * 64 bytes, rank order).
- * Single process (several contexts on one or more devices): link them directly. */
-EPLAB_API int eplab_ipc_handle(eplab_ctx* ctx, void* handle64);
+/* Peer wiring. Multi-process: export my region's record (EPLAB_IPC_HANDLE_BYTES: the CUDA IPC
+ * handle, then a layout signature -- hidden, ffn, experts, topk, world, max_tokens, receive
+ * capacity, device SM count, region size), all-gather the records (NCCL / torch.distributed
+ * bootstrap) and import them (world records, rank order). eplab_connect_ipc returns 2 when any
+ * peer's layout differs (its peer pointers and the senders' slot writes would be wrong).
+ * Single process (several contexts on one or more devices): link them directly (same check). */
+#define EPLAB_IPC_HANDLE_BYTES 128
+EPLAB_API int eplab_ipc_handle(eplab_ctx* ctx, void* handle);
 EPLAB_API int eplab_connect_ipc(eplab_ctx* ctx, const void* handles);
 EPLAB_API int eplab_connect_local(eplab_ctx* const* ctxs, int n);
 
@@ -140,13 +144,24 @@ EPLAB_API int eplab_set_auto_tune(eplab_ctx* ctx, int on);
  * rows through the TMA bulk-copy engine (comm CTAs only) instead of warp copies. Results are
  * bitwise identical for every setting. */
 EPLAB_API int eplab_set_comm_options(eplab_ctx* ctx, int spare_warps, int bulk_mover);
+/* Experiment knobs (A/B measurements; never read from the environment): "engine_pair" (1: CTA-pair
+ * engine, 0: single-CTA), "spare" / "comm_bulk" (as eplab_set_comm_options), "rgp" / "tngp" /
+ * "tngp_d" (raster groups of the NT / up-TN / down-TN pair tiles), "bwd_disp_scale" (comm CTAs of
+ * the backward dispatch relative to the forward's), "dbg" (debug bits that SKIP work: results
+ * wrong, for measuring a role's share only). Unknown names return 2. */
+EPLAB_API int eplab_set_option(eplab_ctx* ctx, const char* name, int value);
 /* Persistent grid size (default: all SMs). Several ranks sharing one GPU (the single-device
  * multi-rank test mode) each get a disjoint budget so their MegaKernels are co-resident. */
 EPLAB_API int eplab_set_sm_budget(eplab_ctx* ctx, int n_sm);
 
 /* Device token map (Alg. 1 + count AllGather + priority schedule), token_map.hpp:68 and :88.
  * d_topk_ids int32 [n_tok][topk], d_gate_w fp32 [n_tok][topk]; both must stay valid until
- * the backward calls of this iteration. Starts a new iteration (epoch). */
+ * the backward calls of this iteration. Starts a new iteration (epoch).
+ * On the device the planner applies validate_routing's checks (types.cpp:74-94: expert id in
+ * [0, E), distinct experts per token, finite gate weights) and checks the receive capacity of
+ * EVERY rank (max_recv_rows). A failure on any rank aborts the iteration on all ranks -- every
+ * kernel of it returns without reading or writing rows -- and eplab_check reports 2 with the
+ * reason (the host cannot see device routing without a synchronisation). */
 EPLAB_API int eplab_plan(eplab_ctx* ctx, const int32_t* d_topk_ids, const float* d_gate_w,
                          int n_tok, void* stream);
 
@@ -196,8 +211,10 @@ EPLAB_API int eplab_moe_step_host_async(eplab_ctx* ctx, const int32_t* h_topk_id
 /* Makes `stream` wait (on the device) for every enqueued host-step copy. */
 EPLAB_API int eplab_host_join(eplab_ctx* ctx, void* stream);
 
-/* Synchronises `stream` and reports the device error word: 0 ok, 2 capacity exceeded,
- * 3 scoreboard watchdog fired (DeadlockError analogue, error.hpp:19-22). Clears it. */
+/* Synchronises `stream` and reports the device error word: 0 ok, 2 the iteration was aborted by
+ * the planner's checks (bad routing on some rank, or a rank's receive capacity exceeded), 3 a
+ * scoreboard watchdog fired (DeadlockError analogue, error.hpp:19-22; the message names the wait
+ * site). Clears it. Until it is cleared every later kernel of the context skips its work. */
 EPLAB_API int eplab_check(eplab_ctx* ctx, void* stream);
 
 /* Bit-exact exports of the device token map (synchronising). Arrays of n_tok*topk entries;
@@ -216,6 +233,36 @@ EPLAB_API void* eplab_buffer(eplab_ctx* ctx, const char* name);
  * the reference's Chrome-trace format (trace.cpp:13-34). cap = 0 disables. */
 EPLAB_API int eplab_timeline_enable(eplab_ctx* ctx, int cap);
 EPLAB_API int eplab_timeline_export(eplab_ctx* ctx, const char* path, double* overlap_frac);
+
+/* ------------------------------------------ unfused baseline
+ * NCCL all-to-all -> grouped GEMM (+SwiGLU) -> NCCL all-to-all back -> k-order reduce, as separate
+ * kernels with the caller's collectives in between (host-synchronised split sizes, no overlap).
+ * The GEMM tiles are the MegaKernels' own (same engine, epilogues, K order) with the collectives
+ * removed and the fold is the MegaKernels' fold, so a step through these entry points is BITWISE
+ * equal to the fused step: the reference's fused_vs_sequential contract (precision.cpp:54-96).
+ * Per step and rank (A2A = the caller's all-to-all, rows as the first dimension):
+ *   plan_counts(row[E+1]) ; AllGather rows -> rows_all[W][E+1] ; plan_finish(rows_all)
+ *   pack(x, send, send_meta[n][2]) ; A2A(send, send_meta) ; scatter(recv, recv_meta, n_recv, 0)
+ *   up(w_up) ; down(w_down, o_ret[n_recv]) ; A2A back -> o_src[n_send] ; combine(o_src, y, 0)
+ *   pack(dy, send, NULL) ; A2A ; scatter(recv, NULL, n_recv, 1) ; dgate(dy, o_src, dgate)
+ *   bwd_down(w_down, dw_down) ; bwd_up(w_up, dx_ret, dw_up) ; A2A back -> dx_src ; combine(dx_src, dx, 1)
+ * Send split to rank d = sum of rows_all[me][d*epr .. d*epr+epr); receive split from rank s = sum of
+ * rows_all[s][me*epr .. me*epr+epr). Paper_2604_19241_b200/unfused.py drives it over NCCL. */
+EPLAB_API int eplab_unfused_plan_counts(eplab_ctx* ctx, const int32_t* d_topk_ids, const float* d_gate_w,
+                                        int n_tok, int32_t* d_row, void* stream);
+EPLAB_API int eplab_unfused_plan_finish(eplab_ctx* ctx, const int32_t* d_rows_all, void* stream);
+EPLAB_API int eplab_unfused_pack(eplab_ctx* ctx, const void* d_src, void* d_send, int32_t* d_send_meta,
+                                 void* stream);
+EPLAB_API int eplab_unfused_scatter(eplab_ctx* ctx, const void* d_recv, const int32_t* d_recv_meta, int n_recv,
+                                    int phase, void* stream);
+EPLAB_API int eplab_unfused_up(eplab_ctx* ctx, const void* d_w_up, void* stream);
+EPLAB_API int eplab_unfused_down(eplab_ctx* ctx, const void* d_w_down, void* d_o_ret, void* stream);
+EPLAB_API int eplab_unfused_combine(eplab_ctx* ctx, const void* d_rows, void* d_out, int phase, void* stream);
+EPLAB_API int eplab_unfused_dgate(eplab_ctx* ctx, const void* d_dy, const void* d_o_rows, float* d_dgate,
+                                  void* stream);
+EPLAB_API int eplab_unfused_bwd_down(eplab_ctx* ctx, const void* d_w_down, void* d_dw_down, void* stream);
+EPLAB_API int eplab_unfused_bwd_up(eplab_ctx* ctx, const void* d_w_up, void* d_dx_ret, void* d_dw_up,
+                                   void* stream);
 
 /* ------------------------------------------------ host model API (C view of eplab::, eplab.hpp) */
 
@@ -255,6 +302,12 @@ EPLAB_API int eplab_sample_routing(int n_exp, int topk, long long n_tok, int wor
 EPLAB_API int eplab_host_token_map(const int32_t* sel, int world, int n_exp, long long n_tok,
                                    int topk, int32_t* target_rank, int32_t* local_expert,
                                    int64_t* offset, int64_t* recv_totals, int64_t* seg_base);
+/* One rank's part of build_global_token_map, as each rank computes it in an EP run: its own
+ * routing sel [n_tok*topk] (local stable sort, Alg. 1 l.1-2) and the all-gathered per-expert
+ * counts of every rank counts_all [world][n_exp] (l.3) give its map entries (l.4-16). */
+EPLAB_API int eplab_host_rank_token_map(const int32_t* sel, const int64_t* counts_all, int rank, int world,
+                                        int n_exp, long long n_tok, int topk, int32_t* target_rank,
+                                        int32_t* local_expert, int64_t* offset);
 /* build_send_schedule (token_map.hpp:88) for one rank. */
 EPLAB_API int eplab_host_send_schedule(const int32_t* sel, int world, int n_exp, long long n_tok,
                                        int topk, int rank, int64_t* item_token, int32_t* item_slot,

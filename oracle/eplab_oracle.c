@@ -597,16 +597,17 @@ int orc_moe_layer(const orc_layer_dims* d, const int32_t* sel, const float* gw,
       orow[nn] = tobf(acc);
     }
   }
-  /* combine: k-ascending fmaf fold, one RNE at the end */
+  /* combine: the reference's canonical fold (precision.cpp:31-37, FpFormat::Binary32: acc = w0*v0,
+   * acc = acc + wj*vj, j ascending, fp32 rounding of every product and sum), one RNE at the end */
   if (y) {
 #pragma omp parallel for
-    for (long long rt = 0; rt < (long long)W * T; ++rt)
+    for (long long rt = 0; rt < (long long)W * T; ++rt) {
+      float v[32];
       for (int nn = 0; nn < H; ++nn) {
-        float acc = 0.0f;
-        for (int j = 0; j < K; ++j)
-          acc = fmaf(gw[rt * K + j], bf(o[(size_t)pos[rt * K + j] * H + nn]), acc);
-        y[(size_t)rt * H + nn] = tobf(acc);
+        for (int j = 0; j < K; ++j) v[j] = bf(o[(size_t)pos[rt * K + j] * H + nn]);
+        y[(size_t)rt * H + nn] = tobf(orc_fold(gw + rt * K, v, K, 0));
       }
+    }
   }
   if (!dy) goto done;
   {
@@ -640,13 +641,16 @@ int orc_moe_layer(const orc_layer_dims* d, const int32_t* sel, const float* gw,
       }
     }
     if (dx) {
+      /* the same fold with unit weights: dx = bf16(dX_0 + dX_1 + ...) in j order */
 #pragma omp parallel for
-      for (long long rt = 0; rt < (long long)W * T; ++rt)
+      for (long long rt = 0; rt < (long long)W * T; ++rt) {
+        float v[32], one[32];
+        for (int j = 0; j < K; ++j) one[j] = 1.0f;
         for (int k = 0; k < H; ++k) {
-          float acc = 0.0f;
-          for (int j = 0; j < K; ++j) acc = acc + bf(dxr[(size_t)pos[rt * K + j] * H + k]);
-          dx[(size_t)rt * H + k] = tobf(acc);
+          for (int j = 0; j < K; ++j) v[j] = bf(dxr[(size_t)pos[rt * K + j] * H + k]);
+          dx[(size_t)rt * H + k] = tobf(orc_fold(one, v, K, 0));
         }
+      }
     }
     if (dgate) {
 #pragma omp parallel for

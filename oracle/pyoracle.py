@@ -212,15 +212,16 @@ class Oracle(_Lib):
         return best, lmin.value, ev.value
 
     def moe_layer(self, world, n_exp, topk, H, F, sel, gw, x, w_up, w_down, dy, threads=0,
-                  want_grads=True):
-        """bf16 tensors as uint16 numpy arrays. Returns dict of outputs."""
+                  want_grads=True, want_dw=True):
+        """bf16 tensors as uint16 numpy arrays. Returns dict of outputs (want_dw=False skips the
+        weight gradients: the row-local outputs of a token sample need only its rows)."""
         n_tok = sel.shape[1] // topk
         d = LayerDims(world, n_exp, topk, H, F, n_tok)
         y = np.zeros((world, n_tok, H), np.uint16)
         dx = np.zeros((world, n_tok, H), np.uint16) if want_grads else None
         dg = np.zeros((world, n_tok * topk), np.float32) if want_grads else None
-        dwu = np.zeros((n_exp, 2 * F, H), np.uint16) if want_grads else None
-        dwd = np.zeros((n_exp, H, F), np.uint16) if want_grads else None
+        dwu = np.zeros((n_exp, 2 * F, H), np.uint16) if (want_grads and want_dw) else None
+        dwd = np.zeros((n_exp, H, F), np.uint16) if (want_grads and want_dw) else None
         arrs = [np.ascontiguousarray(a) for a in (sel.astype(np.int32), gw.astype(np.float32), x, w_up,
                                                   w_down)]
         dyc = np.ascontiguousarray(dy) if (dy is not None and want_grads) else None

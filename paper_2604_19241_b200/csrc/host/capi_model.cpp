@@ -118,6 +118,38 @@ int eplab_host_token_map(const int32_t* sel, int world, int n_exp, long long n_t
   });
 }
 
+int eplab_host_rank_token_map(const int32_t* sel, const int64_t* counts_all, int rank, int world,
+                              int n_exp, long long n_tok, int topk, int32_t* target_rank,
+                              int32_t* local_expert, int64_t* offset) {
+  return guarded([&] {
+    if (world < 1 || n_exp % world) throw ValidationError("n_exp not divisible by world");
+    if (rank < 0 || rank >= world) throw ValidationError("rank out of range");
+    // this rank's routing alone (Alg. 1 l.1-2) + every rank's counts (l.3) -> its map (l.4-16)
+    RoutingInstance one;
+    one.world = 1;
+    one.n_exp = n_exp;
+    one.topk = topk;
+    one.n_tok = n_tok;
+    one.selected_experts.assign(1, std::vector<int>(sel, sel + (size_t)n_tok * topk));
+    one.gate_weights.assign(1, std::vector<float>((size_t)n_tok * topk, 1.0f));
+    validate_routing(one);
+    const LocalSortResult loc = local_stable_sort(one.selected_experts[0], n_tok, topk, n_exp);
+    std::vector<std::vector<long long>> counts(world, std::vector<long long>(n_exp));
+    for (int r = 0; r < world; ++r)
+      for (int e = 0; e < n_exp; ++e) counts[r][e] = counts_all[(size_t)r * n_exp + e];
+    if (counts[rank] != loc.expert_counts)
+      throw ValidationError("all_expert_counts row of this rank differs from its own routing");
+    const GlobalOffsets oall = compute_global_offsets(counts, world, n_exp);
+    const int epr = n_exp / world;
+    for (size_t i = 0; i < loc.m_loc.size(); ++i) {
+      const int e = one.selected_experts[0][i];
+      target_rank[i] = e / epr;
+      local_expert[i] = e % epr;
+      offset[i] = loc.m_loc[i] - loc.expert_offsets[e] + oall.at(e / epr, e % epr, rank);
+    }
+  });
+}
+
 int eplab_host_send_schedule(const int32_t* sel, int world, int n_exp, long long n_tok, int topk,
                              int rank, int64_t* item_token, int32_t* item_slot,
                              int32_t* item_dst_rank, int32_t* item_dst_expert,

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -80,10 +81,23 @@ struct eplab_ctx {
   // comm pool workers: spare GEMM warps join (warp split; EPLAB_SPARE=0 disables), bulk-copy
   // mover instead of warp copies (EPLAB_COMM=bulk); eplab_set_comm_options overrides both
   int spare_warps = 3, comm_bulk = 0;
+  // experiment knobs (eplab_set_option; never read from the environment): raster groups of the
+  // NT / TN pair tiles, backward comm-CTA scale, debug bits (dbg != 0 gives WRONG results)
+  int rgp = 8, tngp = 4, tngp_d = 4, bwd_disp_scale = 2, dbg = 0;
+  // EP > 1: relay on/off is a protocol choice every rank must share; fixed at init from the
+  // shape and the device (identical on every rank, checked by the IPC layout signature)
+  int relay_pref = -1, relay_pref_n = 0, dev_sms = 148;
   // auto-tune (default until eplab_set_tune_config): per 4096-token bucket of n_tok, the
   // B200 model's search_layer result (the reference TuneCache's bucketing, tuner.cpp:150-165)
   bool auto_tune = true;
   std::map<long long, eplab_tune_config> tune_cache;
+  // unfused baseline scratch (eplab_unfused_*; allocated on first use): send position of every
+  // routing entry [T_max*k], return position of every receive slot [M_cap], the count row for
+  // the host's all-gather [E+1], and the all-gathered rows of the current plan (caller's buffer)
+  int* uf_spos = nullptr;
+  int* uf_ret_pos = nullptr;
+  int* uf_counts = nullptr;
+  const int* uf_call = nullptr;
   // timeline
   TimelineRec* tl_rec = nullptr;
   int* tl_count = nullptr;
@@ -104,6 +118,34 @@ SymPtrs sym_ptrs(const eplab_ctx* c, char* base) {
   s.tok_cnt = reinterpret_cast<uint32_t*>(base + c->off_tok);
   s.cnt_all = reinterpret_cast<int*>(base + c->off_cnt_all);
   s.cnt_flag = reinterpret_cast<uint32_t*>(base + c->off_cnt_flag);
+  return s;
+}
+
+// Layout signature exchanged with the IPC handle (bytes 64..127 of an EPLAB_IPC_HANDLE_BYTES
+// record): everything the peer-pointer arithmetic and the senders' slot/counter writes depend on.
+struct LayoutSig {
+  int64_t sym_bytes;
+  int32_t H, F, E, topk, world, T_max, M_cap, dev_sms, relay_pref, pad[5];
+  std::string describe() const {
+    return "H=" + std::to_string(H) + " F=" + std::to_string(F) + " E=" + std::to_string(E) +
+           " k=" + std::to_string(topk) + " W=" + std::to_string(world) + " T_max=" +
+           std::to_string(T_max) + " M_cap=" + std::to_string(M_cap) + " SMs=" +
+           std::to_string(dev_sms) + " relay=" + std::to_string(relay_pref);
+  }
+};
+static_assert(sizeof(LayoutSig) == 64, "layout signature must fill the second 64 bytes");
+LayoutSig layout_sig(const eplab_ctx* c) {
+  LayoutSig s{};
+  s.sym_bytes = (int64_t)c->sym_bytes;
+  s.H = c->d.H;
+  s.F = c->d.F;
+  s.E = c->d.E;
+  s.topk = c->d.topk;
+  s.world = c->d.world;
+  s.T_max = c->d.T_max;
+  s.M_cap = c->d.M_cap;
+  s.dev_sms = c->dev_sms;
+  s.relay_pref = c->relay_pref;
   return s;
 }
 
@@ -143,28 +185,101 @@ MkArgs base_args(eplab_ctx* c) {
   a.n_red = std::max(1, c->cfg.n_red);
   a.timeout_ns = c->timeout_ns;
   a.tl = Timeline{c->tl_rec, c->tl_count, c->tl_cap};
-  a.dbg = getenv("EPLAB_DBG") ? atoi(getenv("EPLAB_DBG")) : 0;
+  a.dbg = c->dbg;
   a.pair = c->pair;
   a.comm_bulk = c->comm_bulk;
   a.comm_cursor = c->cursor + 2;
   a.red_cursor = reinterpret_cast<unsigned*>(c->cursor + 4);
   a.relay_cursor = reinterpret_cast<unsigned*>(c->cursor + 5);
   a.spare_warps = c->spare_warps;
-  // A/B experiments: environment switches read per launch
-  if (const char* e = getenv("EPLAB_COMM")) a.comm_bulk = std::string(e) == "bulk";
-  if (const char* e = getenv("EPLAB_SPARE")) a.spare_warps = atoi(e);
-  a.rgp = getenv("EPLAB_RGP") ? std::max(1, atoi(getenv("EPLAB_RGP"))) : 8;
-  a.tngp = getenv("EPLAB_TNGP") ? std::max(1, atoi(getenv("EPLAB_TNGP"))) : 4;
-  a.tngp_d = getenv("EPLAB_TNGP_D") ? std::max(1, atoi(getenv("EPLAB_TNGP_D"))) : 4;  // profiles/r01_wgrad_raster.txt
+  a.rgp = c->rgp;
+  a.tngp = c->tngp;
+  a.tngp_d = c->tngp_d;  // profiles/r01_wgrad_raster.txt
   // somebody must move the rows: the bulk mover and spare-less pools need >= 1 comm CTA
   if (a.n_disp == 0 && (a.comm_bulk || !(a.spare_warps & 1))) a.n_disp = 1;
   return a;
+}
+
+// Names of the scoreboard wait sites reported by the watchdog (err[1] of an error 3).
+std::string wait_site_name(int site) {
+  switch (site) {
+    case 1: return "the count AllGather of eplab_plan (a peer's planner never published its counts)";
+    case 10: case 11: return "a relay worker's slot-flag wait (dispatch rows of a peer never landed)";
+    case 20: case 21: return "a reduce worker's top-k barrier (combine replicas never arrived)";
+    case 30: return "an up-GEMM tile's rowgroup wait (forward dispatch rows never landed)";
+    case 31: return "a down-dgrad tile's rowgroup wait (backward dispatch rows never landed)";
+    case 32: return "a down-wgrad tile's wait for its dgrad tiles";
+    default: return site >= 40 && site < 48 ? "the GEMM engine's pipeline barriers" : "an unknown wait";
+  }
+}
+
+// Error 2 of an aborted iteration (plan_global_kernel: err[1] = reason bits, err[2] = rank,
+// err[3] = rows needed / capacity, err[4] = first offending routing entry). The reference raises
+// the same conditions as ValidationError from validate_routing (types.cpp:74-94).
+std::string abort_message(const int* ev) {
+  const int bits = ev[1];
+  std::string m;
+  if (bits & 1) m += "selected_experts: expert id out of range; ";
+  if (bits & 2) m += "selected_experts: duplicate expert within token; ";
+  if (bits & 4) m += "gate_weights: non-finite weight; ";
+  if (bits & 7)
+    m += "(routing entry " + std::to_string(ev[4]) + " of this rank, t*topk+j); ";
+  if (bits & 32) m += "routing of rank " + std::to_string(ev[2]) + " failed its checks; ";
+  if (bits & 8)
+    m += "receive capacity exceeded on rank " + std::to_string(ev[2]) + ": " + std::to_string(ev[3]) +
+         " aligned rows needed (max_recv_rows too small); ";
+  if (m.empty()) m = "iteration aborted; ";
+  return "ValidationError: " + m + "the iteration was skipped (no rows were sent)";
 }
 
 void require_plan(eplab_ctx* c) {
   validate(c->planned, "no plan: call eplab_plan (or eplab_moe_fwd) first");
 }
 
+}  // namespace
+
+namespace {
+eplab_tune_config search_config(eplab_ctx* c, long long bucket);
+
+// Launch parameters for this context's shape at n_tok tokens per rank: search_layer over the B200
+// model at the bucket's upper edge, n_red = every SM, and the measured floor on comm CTAs the model
+// does not capture (16 with the spare-warp comm workers, 64 without, scaled by the SM budget;
+// profiles/r01_spare_warps.txt). Cached per 4096-token bucket.
+eplab_tune_config auto_config(eplab_ctx* c, int n_tok) {
+  const long long bucket = eplab::token_bucket(std::max(1, n_tok));
+  auto it = c->tune_cache.find(bucket);
+  if (it != c->tune_cache.end()) return it->second;
+  eplab_tune_config cfg = search_config(c, bucket);
+  if (c->d.world > 1 && (c->relay_pref > 0) != (cfg.n_relay > 0)) {
+    // relay on/off is a protocol choice every rank must share (a sender's dedup needs the
+    // receiver's relay): fixed at eplab_init from the max_tokens bucket at the device's SM count
+    // and the default comm workers -- identical on every rank, whatever its n_tok, SM budget or
+    // comm options; only the SM split follows this rank's n_tok
+    cfg.n_relay = c->relay_pref > 0 ? std::max(1, c->relay_pref_n * c->num_sms / c->dev_sms) : 0;
+    if (cfg.n_disp + cfg.n_relay >= c->num_sms) cfg.n_disp = std::max(0, c->num_sms - cfg.n_relay - 1);
+  }
+  c->tune_cache[bucket] = cfg;
+  return cfg;
+}
+
+eplab_tune_config search_config(eplab_ctx* c, long long bucket) {
+  eplab::MoEShape shape;
+  shape.name = "ctx";
+  shape.h_dim = c->d.H;
+  shape.h_inter = c->d.F;
+  shape.n_exp = c->d.E;
+  shape.topk = c->d.topk;
+  shape.n_tok = bucket * 4096;
+  eplab::HardwareSpec hw = eplab::b200_hardware(c->d.world);
+  hw.n_sm = c->num_sms;
+  eplab::B200Calib calib;
+  if (!(c->spare_warps & 1)) calib.spare_sm_equiv = 0;
+  const eplab::TuneResult r = eplab::search_layer(hw, shape, 0, calib);
+  eplab_tune_config cfg{r.best.n_disp, r.best.n_relay, 1, c->num_sms, 8};
+  const int floor = ((c->spare_warps & 1) ? 16 : 64) * c->num_sms / 148;
+  if (cfg.n_disp < floor && floor + cfg.n_relay < c->num_sms) cfg.n_disp = floor;
+  return cfg;
+}
 }  // namespace
 
 extern "C" {
@@ -202,7 +317,7 @@ int eplab_init(const eplab_init_args* args, eplab_ctx** out) {
     d.M_cap = (int)mcap;
     d.RG_cap = d.M_cap / kBM;
     c->cfg.n_red = c->num_sms;
-    if (const char* eng = getenv("EPLAB_ENGINE")) c->pair = std::string(eng) != "single";
+    c->dev_sms = c->num_sms;
 
     // ---- symmetric region
     size_t o = 0;
@@ -267,6 +382,10 @@ int eplab_init(const eplab_init_args* args, eplab_ctx** out) {
     c->cursor = reinterpret_cast<int*>(c->loc + o_cur);
     c->err = reinterpret_cast<int*>(c->loc + o_err);
     c->epoch_dev = reinterpret_cast<uint32_t*>(c->loc + o_ep);
+    {  // planner scratch: scalars[5] = first offending routing entry (running minimum)
+      const int first_bad = INT_MAX;
+      CK(cudaMemcpy(p.scalars + 5, &first_bad, 4, cudaMemcpyHostToDevice));
+    }
 
     // ---- host-call staging (allocated on the first host call): ids, gate weights, x, dy, y,
     // dx, dgate
@@ -295,6 +414,11 @@ int eplab_init(const eplab_init_args* args, eplab_ctx** out) {
     c->st_hact = eplab_host::make_store_map(c->hact, M, d.F);
     c->st_dgu = eplab_host::make_store_map(c->dgu, M, 2 * d.F);
     c->st_hw = eplab_host::make_store_map(c->hw, M, d.F);
+    if (W > 1) {
+      const eplab_tune_config ref = search_config(c, eplab::token_bucket(d.T_max));
+      c->relay_pref = ref.n_relay > 0 ? 1 : 0;
+      c->relay_pref_n = ref.n_relay;
+    }
     if (eplab_launch::preload_megakernels() || eplab_launch::preload_plan())
       throw Fail{EPLAB_ERR_INTERNAL, std::string("kernel preload: ") + cudaGetErrorString(cudaGetLastError())};
     CK(cudaDeviceSynchronize());
@@ -320,16 +444,19 @@ int eplab_destroy(eplab_ctx* c) {
   }
   if (c->tl_rec) cudaFree(c->tl_rec);
   if (c->tl_count) cudaFree(c->tl_count);
+  if (c->uf_spos) cudaFree(c->uf_spos);
   delete c;
   return EPLAB_OK;
 }
 
-int eplab_ipc_handle(eplab_ctx* c, void* handle64) {
+int eplab_ipc_handle(eplab_ctx* c, void* handle) {
   return guarded([&] {
     cudaIpcMemHandle_t h;
     CK(cudaIpcGetMemHandle(&h, c->sym));
     static_assert(sizeof(h) == 64, "ipc handle size");
-    std::memcpy(handle64, &h, 64);
+    std::memcpy(handle, &h, 64);
+    const LayoutSig sig = layout_sig(c);
+    std::memcpy(static_cast<char*>(handle) + 64, &sig, sizeof(sig));
   });
 }
 
@@ -337,13 +464,26 @@ int eplab_connect_ipc(eplab_ctx* c, const void* handles) {
   return guarded([&] {
     CK(cudaSetDevice(c->device));
     const char* hs = static_cast<const char*>(handles);
+    // every peer's symmetric region must have this rank's layout: the peer pointers below are
+    // this rank's offsets applied to the peer's base, and M_cap / T_max bound the slots and
+    // counters the senders write (a mismatch would corrupt peer memory)
+    const LayoutSig mine = layout_sig(c);
+    for (int r = 0; r < c->d.world; ++r) {
+      LayoutSig s;
+      std::memcpy(&s, hs + EPLAB_IPC_HANDLE_BYTES * r + 64, sizeof(s));
+      validate(std::memcmp(&s, &mine, sizeof(s)) == 0,
+               "rank " + std::to_string(r) + "'s symmetric layout differs from rank " +
+                   std::to_string(c->d.rank) + "'s (" + s.describe() + " vs " + mine.describe() +
+                   "): every rank needs the same hidden, ffn, n_experts, topk, world, max_tokens, "
+                   "max_recv_rows and device");
+    }
     for (int r = 0; r < c->d.world; ++r) {
       if (r == c->d.rank) {
         c->peers.p[r] = c->mine;
         continue;
       }
       cudaIpcMemHandle_t h;
-      std::memcpy(&h, hs + 64 * r, 64);
+      std::memcpy(&h, hs + EPLAB_IPC_HANDLE_BYTES * r, 64);
       void* p = nullptr;
       CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
       c->ipc_opened.push_back(p);
@@ -357,7 +497,9 @@ int eplab_connect_local(eplab_ctx* const* ctxs, int n) {
     validate(n >= 1 && n <= MAX_WORLD, "bad context count");
     for (int i = 0; i < n; ++i) {
       validate(ctxs[i]->d.world == n && ctxs[i]->d.rank == i, "contexts must be ranks 0..n-1");
-      validate(ctxs[i]->sym_bytes == ctxs[0]->sym_bytes, "contexts must be symmetric");
+      const LayoutSig a = layout_sig(ctxs[i]), b = layout_sig(ctxs[0]);
+      validate(std::memcmp(&a, &b, sizeof(a)) == 0,
+               "contexts must be symmetric (" + a.describe() + " vs " + b.describe() + ")");
     }
     for (int i = 0; i < n; ++i) {
       cudaSetDevice(ctxs[i]->device);
@@ -414,56 +556,35 @@ int eplab_set_comm_options(eplab_ctx* c, int spare_warps, int bulk_mover) {
   });
 }
 
+int eplab_set_option(eplab_ctx* c, const char* name, int value) {
+  return guarded([&] {
+    validate(c && name, "null argument");
+    const std::string n(name);
+    if (n == "engine_pair") {
+      c->pair = value != 0;
+    } else if (n == "spare") {
+      validate(value >= 0 && value <= 3, "spare must be a bit set in [0, 3]");
+      c->spare_warps = value;
+      c->tune_cache.clear();
+    } else if (n == "comm_bulk") {
+      c->comm_bulk = value != 0;
+      c->tune_cache.clear();
+    } else if (n == "rgp" || n == "tngp" || n == "tngp_d" || n == "bwd_disp_scale") {
+      validate(value >= 1 && value <= 64, n + " must be in [1, 64]");
+      (n == "rgp" ? c->rgp : n == "tngp" ? c->tngp : n == "tngp_d" ? c->tngp_d : c->bwd_disp_scale) = value;
+    } else if (n == "dbg") {
+      c->dbg = value;  // experiments only: non-zero bits skip work and give wrong results
+    } else {
+      validate(false, "unknown option '" + n + "'");
+    }
+  });
+}
+
 int eplab_get_tune_config(const eplab_ctx* c, eplab_tune_config* cfg) {
   *cfg = c->cfg;
   return EPLAB_OK;
 }
 
-namespace {
-// Launch parameters for this context's shape at n_tok tokens per rank: search_layer over the B200
-// model at the bucket's upper edge, n_red = every SM, and the measured floor on comm CTAs the model
-// does not capture (16 with the spare-warp comm workers, 64 without, scaled by the SM budget;
-// profiles/r01_spare_warps.txt). Cached per 4096-token bucket.
-eplab_tune_config search_config(eplab_ctx* c, long long bucket);
-
-eplab_tune_config auto_config(eplab_ctx* c, int n_tok) {
-  const long long bucket = eplab::token_bucket(std::max(1, n_tok));
-  auto it = c->tune_cache.find(bucket);
-  if (it != c->tune_cache.end()) return it->second;
-  eplab_tune_config cfg = search_config(c, bucket);
-  if (c->d.world > 1) {
-    // relay on/off is a protocol choice every rank must share (a sender's dedup needs the
-    // receiver's relay): take it from the max_tokens bucket, identical on every rank; only the
-    // SM split follows this rank's n_tok
-    const eplab_tune_config ref = search_config(c, eplab::token_bucket(c->d.T_max));
-    if ((ref.n_relay > 0) != (cfg.n_relay > 0)) {
-      cfg.n_relay = ref.n_relay;
-      if (cfg.n_disp + cfg.n_relay >= c->num_sms) cfg.n_disp = ref.n_disp;
-    }
-  }
-  c->tune_cache[bucket] = cfg;
-  return cfg;
-}
-
-eplab_tune_config search_config(eplab_ctx* c, long long bucket) {
-  eplab::MoEShape shape;
-  shape.name = "ctx";
-  shape.h_dim = c->d.H;
-  shape.h_inter = c->d.F;
-  shape.n_exp = c->d.E;
-  shape.topk = c->d.topk;
-  shape.n_tok = bucket * 4096;
-  eplab::HardwareSpec hw = eplab::b200_hardware(c->d.world);
-  hw.n_sm = c->num_sms;
-  eplab::B200Calib calib;
-  if (!(c->spare_warps & 1)) calib.spare_sm_equiv = 0;
-  const eplab::TuneResult r = eplab::search_layer(hw, shape, 0, calib);
-  eplab_tune_config cfg{r.best.n_disp, r.best.n_relay, 1, c->num_sms, 8};
-  const int floor = ((c->spare_warps & 1) ? 16 : 64) * c->num_sms / 148;
-  if (cfg.n_disp < floor && floor + cfg.n_relay < c->num_sms) cfg.n_disp = floor;
-  return cfg;
-}
-}  // namespace
 
 int eplab_set_auto_tune(eplab_ctx* c, int on) {
   return guarded([&] {
@@ -543,7 +664,7 @@ int eplab_dispatch_group_gemm_bwd(eplab_ctx* c, const void* dy, const void* w_do
     // the backward dispatch moves twice the bytes of the forward one (dY rows plus the o rows
     // of the gate gradient): twice the comm CTAs, within the deadlock constraint
     // (profiles/r01_ndisp_sweep_bwd.txt)
-    const int scale = getenv("EPLAB_BWD_DISP_SCALE") ? std::max(1, atoi(getenv("EPLAB_BWD_DISP_SCALE"))) : 2;
+    const int scale = c->bwd_disp_scale;
     a.n_disp = std::max(a.n_disp, std::min(a.n_disp * scale, c->num_sms / 2 - a.n_relay));
     a.dy = static_cast<const __nv_bfloat16*>(dy);
     a.w_down = static_cast<const __nv_bfloat16*>(w_down);
@@ -671,6 +792,8 @@ int eplab_moe_step_host(eplab_ctx* c, const int32_t* h_ids, const float* h_gw, i
                       (cudaStream_t)stream);
     CK(cudaStreamSynchronize(c->d2h_st));
     CK(cudaStreamSynchronize((cudaStream_t)stream));
+    const int rc = eplab_check(c, stream);
+    if (rc) throw Fail{rc, eplab_host::last_error()};
   });
 }
 
@@ -702,10 +825,11 @@ int eplab_check(eplab_ctx* c, void* stream) {
     const int e = ev[0];
     if (e == 3)
       throw Fail{EPLAB_ERR_DEADLOCK,
-                 "DeadlockDetected: scoreboard watchdog fired (site " + std::to_string(ev[1]) +
-                     ", target " + std::to_string(ev[2]) + ", seen " + std::to_string(ev[3]) +
-                     ", at " + std::to_string(ev[4]) + ")"};
-    if (e == 2) throw Fail{EPLAB_ERR_VALIDATION, "receive capacity exceeded (max_recv_rows)"};
+                 "DeadlockDetected: scoreboard watchdog fired at " + wait_site_name(ev[1]) + " (site " +
+                     std::to_string(ev[1]) + ", target " + std::to_string(ev[2]) + ", seen " +
+                     std::to_string(ev[3]) + ", at " + std::to_string(ev[4]) +
+                     "); the iteration's outputs are invalid and the contexts must be re-created"};
+    if (e == 2) throw Fail{EPLAB_ERR_VALIDATION, abort_message(ev)};
     if (e) throw Fail{EPLAB_ERR_INTERNAL, "device error word " + std::to_string(e)};
   });
 }
@@ -873,6 +997,195 @@ int eplab_timeline_export(eplab_ctx* c, const char* path, double* overlap_frac) 
       m << "overlap_frac," << overlap << "\n";
       m << "records," << n << "\n";
     }
+  });
+}
+
+// ------------------------------------------------------------------ unfused baseline
+namespace {
+void uf_alloc(eplab_ctx* c) {
+  if (c->uf_spos) return;
+  const size_t Tk = (size_t)c->d.T_max * c->d.topk;
+  char* b = nullptr;
+  const size_t o1 = align_up(Tk * 4, 256), o2 = o1 + align_up((size_t)c->d.M_cap * 4, 256);
+  CK(cudaMalloc(&b, o2 + align_up((size_t)(c->d.E + 1) * 4, 256)));
+  c->uf_spos = reinterpret_cast<int*>(b);
+  c->uf_ret_pos = reinterpret_cast<int*>(b + o1);
+  c->uf_counts = reinterpret_cast<int*>(b + o2);
+}
+
+MkArgs uf_args(eplab_ctx* c) {
+  MkArgs a = base_args(c);
+  a.unfused = 1;
+  a.n_disp = a.n_relay = a.n_red = 0;  // GEMM tiles only: no comm, relay or reduce tasks
+  a.spare_warps = 0;
+  a.ret_pos = c->uf_ret_pos;
+  return a;
+}
+
+void uf_require(eplab_ctx* c) {
+  require_plan(c);
+  validate(c->uf_call != nullptr, "unfused: call eplab_unfused_plan_finish first");
+}
+}  // namespace
+
+int eplab_unfused_plan_counts(eplab_ctx* c, const int32_t* ids, const float* gw, int n_tok, int32_t* d_row,
+                              void* stream) {
+  return guarded([&] {
+    validate(n_tok >= 0 && n_tok <= c->d.T_max, "n_tok exceeds max_tokens");
+    CK(cudaSetDevice(c->device));
+    uf_alloc(c);
+    c->epoch++;
+    c->plan.n_tok = n_tok;
+    c->plan.topk_ids = ids;
+    c->plan.gate_w = gw;
+    c->uf_call = nullptr;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (eplab_launch::plan_counts_launch(c->d, c->plan, c->epoch_dev, d_row, st))
+      throw Fail{EPLAB_ERR_INTERNAL, std::string("plan counts: ") + cudaGetErrorString(cudaGetLastError())};
+    c->planned = false;
+  });
+}
+
+int eplab_unfused_plan_finish(eplab_ctx* c, const int32_t* d_rows, void* stream) {
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    if (eplab_launch::plan_layout_ext_launch(c->d, c->plan, d_rows, c->err, st))
+      throw Fail{EPLAB_ERR_INTERNAL, std::string("plan layout: ") + cudaGetErrorString(cudaGetLastError())};
+    eplab_launch::zero_padding_launch(c->d, c->plan, c->mine.recv_x, st);
+    eplab_launch::zero_padding_launch(c->d, c->plan, c->mine.recv_dy, st);
+    CK(cudaGetLastError());
+    c->uf_call = d_rows;
+    c->planned = true;
+  });
+}
+
+int eplab_unfused_pack(eplab_ctx* c, const void* src, void* send, int32_t* send_meta, void* stream) {
+  return guarded([&] {
+    uf_require(c);
+    CK(cudaSetDevice(c->device));
+    if (eplab_launch::unfused_pack_launch(c->d, c->plan, static_cast<const __nv_bfloat16*>(src),
+                                          static_cast<__nv_bfloat16*>(send), reinterpret_cast<int2*>(send_meta),
+                                          c->uf_spos, c->num_sms, (cudaStream_t)stream))
+      throw Fail{EPLAB_ERR_INTERNAL, std::string("unfused pack: ") + cudaGetErrorString(cudaGetLastError())};
+  });
+}
+
+int eplab_unfused_scatter(eplab_ctx* c, const void* recv, const int32_t* recv_meta, int n_recv, int phase,
+                          void* stream) {
+  return guarded([&] {
+    uf_require(c);
+    validate(n_recv >= 0 && n_recv <= c->d.M_cap, "n_recv exceeds the receive capacity");
+    validate(phase == 0 || phase == 1, "phase must be 0 (x) or 1 (dY)");
+    CK(cudaSetDevice(c->device));
+    if (eplab_launch::unfused_scatter_launch(c->d, c->plan, c->uf_call, static_cast<const __nv_bfloat16*>(recv),
+                                             reinterpret_cast<const int2*>(recv_meta), n_recv,
+                                             phase == 0 ? c->mine.recv_x : c->mine.recv_dy, c->mine.meta,
+                                             c->uf_ret_pos, c->num_sms, (cudaStream_t)stream))
+      throw Fail{EPLAB_ERR_INTERNAL, std::string("unfused scatter: ") + cudaGetErrorString(cudaGetLastError())};
+  });
+}
+
+int eplab_unfused_up(eplab_ctx* c, const void* w_up, void* stream) {
+  return guarded([&] {
+    uf_require(c);
+    CK(cudaSetDevice(c->device));
+    MkArgs a = uf_args(c);
+    a.w_up = static_cast<const __nv_bfloat16*>(w_up);
+    TmaSet tm;
+    tm.m[0] = c->tm_recv_x_k;
+    tm.m[1] = eplab_host::make_bf16_map(w_up, (uint64_t)c->d.epr * 2 * c->d.F, c->d.H, c->d.H, 64, 128);
+    tm.m[2] = tm.m[0];
+    tm.m[3] = tm.m[1];
+    tm.m[4] = c->st_gu;
+    tm.m[5] = c->st_hact;
+    tm.m[6] = tm.m[7] = c->st_gu;
+    if (eplab_launch::launch_fwd_dispatch(tm, a, c->num_sms, (cudaStream_t)stream))
+      throw Fail{EPLAB_ERR_INTERNAL, std::string("unfused up: ") + cudaGetErrorString(cudaGetLastError())};
+  });
+}
+
+int eplab_unfused_down(eplab_ctx* c, const void* w_down, void* o_ret, void* stream) {
+  return guarded([&] {
+    uf_require(c);
+    CK(cudaSetDevice(c->device));
+    MkArgs a = uf_args(c);
+    a.w_down = static_cast<const __nv_bfloat16*>(w_down);
+    a.ret = static_cast<__nv_bfloat16*>(o_ret);
+    TmaSet tm;
+    tm.m[0] = c->tm_hact_k;
+    tm.m[1] = eplab_host::make_bf16_map(w_down, (uint64_t)c->d.epr * c->d.H, c->d.F, c->d.F, 64, 256);
+    tm.m[2] = eplab_host::make_bf16_map(w_down, (uint64_t)c->d.epr * c->d.H, c->d.F, c->d.F, 64, 128);
+    tm.m[3] = tm.m[1];
+    tm.m[4] = tm.m[5] = tm.m[6] = tm.m[7] = c->st_gu;
+    if (eplab_launch::launch_fwd_combine(tm, a, c->num_sms, (cudaStream_t)stream))
+      throw Fail{EPLAB_ERR_INTERNAL, std::string("unfused down: ") + cudaGetErrorString(cudaGetLastError())};
+  });
+}
+
+int eplab_unfused_combine(eplab_ctx* c, const void* rows, void* out, int phase, void* stream) {
+  return guarded([&] {
+    uf_require(c);
+    validate(phase == 0 || phase == 1, "phase must be 0 (y) or 1 (dx)");
+    CK(cudaSetDevice(c->device));
+    if (eplab_launch::unfused_fold_launch(c->d, c->plan, static_cast<const __nv_bfloat16*>(rows), c->uf_spos,
+                                          static_cast<__nv_bfloat16*>(out), phase, c->num_sms, (cudaStream_t)stream))
+      throw Fail{EPLAB_ERR_INTERNAL, std::string("unfused fold: ") + cudaGetErrorString(cudaGetLastError())};
+  });
+}
+
+int eplab_unfused_dgate(eplab_ctx* c, const void* dy, const void* o_rows, float* dgate, void* stream) {
+  return guarded([&] {
+    uf_require(c);
+    CK(cudaSetDevice(c->device));
+    if (eplab_launch::unfused_dgate_launch(c->d, c->plan, static_cast<const __nv_bfloat16*>(dy),
+                                           static_cast<const __nv_bfloat16*>(o_rows), c->uf_spos, dgate, c->num_sms,
+                                           (cudaStream_t)stream))
+      throw Fail{EPLAB_ERR_INTERNAL, std::string("unfused dgate: ") + cudaGetErrorString(cudaGetLastError())};
+  });
+}
+
+int eplab_unfused_bwd_down(eplab_ctx* c, const void* w_down, void* dw_down, void* stream) {
+  return guarded([&] {
+    uf_require(c);
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaMemsetAsync(c->wg_cnt, 0, (size_t)c->d.epr * (c->d.F / 256) * 4, st));
+    MkArgs a = uf_args(c);
+    a.w_down = static_cast<const __nv_bfloat16*>(w_down);
+    a.dw_down = static_cast<__nv_bfloat16*>(dw_down);
+    TmaSet tm;
+    tm.m[0] = c->tm_recv_dy_k;
+    tm.m[1] = eplab_host::make_bf16_map(w_down, (uint64_t)c->d.epr * c->d.H, c->d.F, c->d.F, 64, 64);
+    tm.m[2] = c->tm_recv_dy_mn;
+    tm.m[3] = c->tm_hw_mn;
+    tm.m[4] = c->st_dgu;
+    tm.m[5] = c->st_hw;
+    tm.m[6] = eplab_host::make_store_map(dw_down, (uint64_t)c->d.epr * c->d.H, c->d.F);
+    tm.m[7] = tm.m[6];
+    if (eplab_launch::launch_bwd_dispatch(tm, a, c->num_sms, st))
+      throw Fail{EPLAB_ERR_INTERNAL, std::string("unfused bwd down: ") + cudaGetErrorString(cudaGetLastError())};
+  });
+}
+
+int eplab_unfused_bwd_up(eplab_ctx* c, const void* w_up, void* dx_ret, void* dw_up, void* stream) {
+  return guarded([&] {
+    uf_require(c);
+    CK(cudaSetDevice(c->device));
+    MkArgs a = uf_args(c);
+    a.w_up = static_cast<const __nv_bfloat16*>(w_up);
+    a.ret = static_cast<__nv_bfloat16*>(dx_ret);
+    a.dw_up = static_cast<__nv_bfloat16*>(dw_up);
+    TmaSet tm;
+    tm.m[0] = c->tm_dgu_k;
+    tm.m[1] = eplab_host::make_bf16_map(w_up, (uint64_t)c->d.epr * 2 * c->d.F, c->d.H, c->d.H, 64, 64);
+    tm.m[2] = c->tm_dgu_mn;
+    tm.m[3] = c->tm_recv_x_mn;
+    tm.m[4] = tm.m[5] = c->st_dgu;
+    tm.m[6] = eplab_host::make_store_map(dw_up, (uint64_t)c->d.epr * 2 * c->d.F, c->d.H);
+    tm.m[7] = tm.m[6];
+    if (eplab_launch::launch_bwd_combine(tm, a, c->num_sms, (cudaStream_t)stream))
+      throw Fail{EPLAB_ERR_INTERNAL, std::string("unfused bwd up: ") + cudaGetErrorString(cudaGetLastError())};
   });
 }
 

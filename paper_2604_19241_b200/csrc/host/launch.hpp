@@ -10,6 +10,19 @@ int preload_plan();
 int plan_launch(const eplab_dev::Dims& d, const eplab_dev::Peers& peers,
                 const eplab_dev::PlanDev& p, uint32_t* epoch, uint64_t timeout_ns, int* err,
                 cudaStream_t st);
+int plan_counts_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p, uint32_t* epoch, int* out,
+                       cudaStream_t st);
+int plan_layout_ext_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p, const int* call, int* err,
+                           cudaStream_t st);
+int unfused_pack_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p, const __nv_bfloat16* src,
+                        __nv_bfloat16* send, int2* send_meta, int* spos, int sms, cudaStream_t st);
+int unfused_scatter_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p, const int* call,
+                           const __nv_bfloat16* recv, const int2* recv_meta, int n_recv, __nv_bfloat16* dst,
+                           eplab_dev::SlotMeta* meta, int* ret_pos, int sms, cudaStream_t st);
+int unfused_fold_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p, const __nv_bfloat16* rows,
+                        const int* spos, __nv_bfloat16* out, int ph, int sms, cudaStream_t st);
+int unfused_dgate_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p, const __nv_bfloat16* dy,
+                         const __nv_bfloat16* rows, const int* spos, float* dgate, int sms, cudaStream_t st);
 int zero_padding_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p,
                         __nv_bfloat16* recv, cudaStream_t st);
 int launch_fwd_dispatch(const eplab_dev::TmaSet& tm, const eplab_dev::MkArgs& a, int grid,

@@ -68,6 +68,10 @@ void validate_tune_config(const TuneConfig& c, const HardwareSpec& s) {
   if (c.n_red < 1 || c.n_red > s.n_sm) bad("n_red", "must be in [1, n_sm]");
 }
 
+long long derive_expanded_tokens(const MoEShape& shape, int) {
+  return shape.n_tok * shape.topk;  // balanced routing: rows received per rank == rows sent
+}
+
 void validate_routing(const RoutingInstance& r) {
   if (r.world < 1) bad("world", "must be >= 1");
   if ((int)r.selected_experts.size() != r.world || (int)r.gate_weights.size() != r.world)
@@ -213,6 +217,18 @@ std::vector<GlobalTokenMap> build_global_token_map(const RoutingInstance& routin
   return maps;
 }
 
+std::string export_map_table(const std::vector<GlobalTokenMap>& maps) {
+  std::string out = "rank\ttoken\tslot\tdst_rank\tdst_expert\tdst_offset\n";
+  for (const GlobalTokenMap& m : maps)
+    for (size_t i = 0; i < m.entries.size(); ++i) {
+      const MapEntry& e = m.entries[i];
+      out += std::to_string(m.rank) + "\t" + std::to_string(i / m.topk) + "\t" + std::to_string(i % m.topk) +
+             "\t" + std::to_string(e.target_rank) + "\t" + std::to_string(e.local_expert) + "\t" +
+             std::to_string(e.offset) + "\n";
+    }
+  return out;
+}
+
 SendSchedule build_send_schedule(const GlobalTokenMap& map) {
   // bucket base of (e_loc, dst) = exclusive scan in (e_loc, dst) order; position inside the
   // bucket = (t, j) order, which is ascending destination offset (stable local sort)
@@ -232,31 +248,43 @@ SendSchedule build_send_schedule(const GlobalTokenMap& map) {
 }
 
 // ------------------------------------------------------------------ traffic (traffic.cpp)
+BigInt stirling2(int n, int k) {
+  if (n < 0 || k < 0 || k > n || n > 64) throw ValidationError("stirling2 supports 0 <= k <= n <= 64");
+  // Pascal-like triangle of S(i, j) = j S(i-1, j) + S(i-1, j-1), kept as the previous row only
+  std::vector<BigInt> prev(1, BigInt(1));  // S(0, 0) = 1
+  for (int i = 1; i <= n; ++i) {
+    std::vector<BigInt> cur(std::min(i, k) + 1, BigInt(0));
+    for (int j = 1; j < (int)cur.size(); ++j) {
+      const BigInt keep = j < (int)prev.size() ? BigInt(j) * prev[j] : BigInt(0);
+      cur[j] = keep + prev[j - 1];
+    }
+    prev.swap(cur);
+  }
+  return k < (int)prev.size() ? prev[k] : BigInt(0);
+}
+
 DistinctRankDistribution distinct_rank_distribution(int world, int topk) {
   if (world < 1 || topk < 1) throw ValidationError("world and topk must be >= 1");
+  if (topk > 64) throw ValidationError("topk must be <= 64");
   DistinctRankDistribution d;
   d.world = world;
   d.topk = topk;
-  for (int i = 0; i < topk; ++i) d.denominator *= (u128)world;
+  for (int i = 0; i < topk; ++i) d.denominator *= BigInt(world);
   const int xmax = std::min(world, topk);
-  // Stirling numbers of the second kind S(topk, x) by the triangle recurrence
-  std::vector<std::vector<u128>> S(topk + 1, std::vector<u128>(xmax + 1, 0));
-  S[0][0] = 1;
-  for (int n = 1; n <= topk; ++n)
-    for (int x = 1; x <= std::min(n, xmax); ++x) S[n][x] = (u128)x * S[n - 1][x] + S[n - 1][x - 1];
-  u128 check = 0, e_num = 0;
+  // P(X = x) = W (W-1) ... (W-x+1) S(topk, x) / W^topk, exact
+  BigInt check = 0, e_num = 0;
   for (int x = 1; x <= xmax; ++x) {
-    u128 falling = 1;  // C(W, x) * x! = W (W-1) ... (W-x+1)
-    for (int i = 0; i < x; ++i) falling *= (u128)(world - i);
-    const u128 num = falling * S[topk][x];
+    BigInt falling = 1;  // C(W, x) * x!
+    for (int i = 0; i < x; ++i) falling *= BigInt(world - i);
+    const BigInt num = falling * stirling2(topk, x);
     d.numerators.push_back(num);
-    d.probs.push_back((double)num / (double)d.denominator);
+    d.probs.push_back(num.to_double() / d.denominator.to_double());
     check += num;
-    e_num += (u128)x * num;
+    e_num += BigInt(x) * num;
   }
   if (check != d.denominator)
     throw ValidationError("distinct_rank_distribution: probabilities do not sum to 1");
-  d.expectation = (double)e_num / (double)d.denominator;
+  d.expectation = e_num.to_double() / d.denominator.to_double();
   const double closed = world * (1.0 - std::pow(1.0 - 1.0 / world, topk));
   if (std::abs(d.expectation - closed) > 1e-12 * std::max(1.0, closed))
     throw ValidationError("distinct_rank_distribution: expectation mismatch vs closed form");
@@ -302,7 +330,9 @@ TrafficReport volume_exact(const RoutingInstance& r, const MoEShape& shape, cons
   const double copies = (double)r.n_tok * r.world;
   MoEShape s = shape;
   s.n_tok = r.n_tok;
-  return make_volumes(s, r.world, copies > 0 ? distinct / copies : 0.0);
+  TrafficReport rep = make_volumes(s, r.world, copies > 0 ? distinct / copies : 0.0);
+  rep.basis = TrafficReport::Basis::ExactInstance;
+  return rep;
 }
 
 double expected_remote_ranks(int n_exp, int world, int topk) {

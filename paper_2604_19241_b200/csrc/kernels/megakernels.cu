@@ -96,6 +96,14 @@ __device__ __forceinline__ void wait_eq_sys(const uint32_t* p, uint32_t want,
   }
 }
 
+// Entry check of every MegaKernel: the planner aborted this iteration (routing checks, receive
+// capacity of any rank, count-exchange timeout: p.scalars[3]) or an earlier kernel's watchdog fired
+// (sticky until eplab_check). Nothing of the iteration is read or written -- in particular no row
+// is pushed into a peer's symmetric buffers.
+__device__ __forceinline__ bool iteration_aborted(const MkArgs& a) {
+  return *reinterpret_cast<const volatile int*>(a.p.scalars + 3) != 0 || aborted(a.err);
+}
+
 // Local expert of a global 128-row block index g (binary search over mblock_pre).
 __device__ __forceinline__ int expert_of_block(const PlanDev& p, int epr, long long g) {
   int lo = 0, hi = epr - 1;
@@ -228,6 +236,7 @@ __device__ __forceinline__ TileDesc half_tile(const TileDesc& td, uint32_t rank)
 }
 // scoreboard wait of an NT pair tile: both 128-row blocks (the second only if it has rows)
 __device__ __forceinline__ void wait_pair_rows(const MkArgs& a, int ph, const TileDesc& td, int site) {
+  if (a.unfused) return;  // rows scattered before the launch
   const SymPtrs& me = a.peers.p[a.d.rank];
   const int g = td.m0 >> 7;
   wait_geq_sys(rg_counter(me, a.d, ph, PAR(a), g), (uint32_t)min(BM, td.rows), a.timeout_ns, a.err, site, g);
@@ -262,17 +271,6 @@ __device__ __forceinline__ void warp_copy_row(int4* __restrict__ dst, const int4
   for (; c < vecs; c += 32) dst[c] = ld_nc_v4(src + c);
 }
 
-__device__ __forceinline__ float dot8_bf16(const int4& a, const int4& b, float acc) {
-  const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&a);
-  const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&b);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const float2 fa = __bfloat1622float2(ha[q]), fb = __bfloat1622float2(hb[q]);
-    acc = fmaf(fa.x, fb.x, acc);
-    acc = fmaf(fa.y, fb.y, acc);
-  }
-  return acc;
-}
 
 // Comm role. The rows of a slice of the priority-ordered send schedule (token_map.cpp:108-126)
 // are moved by the TMA bulk-copy engine: one elected thread streams them global -> smem slot ->
@@ -704,9 +702,11 @@ __device__ int relay_rowgroups(const MkArgs& a, int ph) {
 __device__ void relay_task(const MkArgs& a, int, int ph) { relay_rowgroups(a, ph); }
 
 // ------------------------------------------------------------------ reduce role
-// Top-k completeness barrier, then the fixed k-ascending fold (
-// precision.cpp:31-37 order): forward y = bf16(fma-fold of w_j * o_j), backward
-// dx = bf16(sum_j dX_j), both in fp32. The fold of one token is a warp job: the token's k
+// Top-k completeness barrier, then the reference's canonical fold (precision.cpp:31-37
+// `fold` with FpFormat::Binary32): acc = w_0 * o_0, acc = acc + w_j * o_j for j ascending, every
+// product and sum rounded to fp32 (no FMA contraction), then one RNE to bf16:
+// y = round_to_bf16(accumulate(plan, Binary32)) bit for bit; backward dx the same fold with unit
+// weights (dx = bf16(dX_0 + dX_1 + ...)). The fold of one token is a warp job: the token's k
 // replica rows are one contiguous block [t*k, t*k+k) x H, each lane keeps KT x U 16-byte loads in
 // flight (KT >= k replicas x U column chunks, 16 per lane), so the HBM-bound fold is not
 // latency-bound.
@@ -744,13 +744,12 @@ __device__ __forceinline__ void fold_token(const MkArgs& a, int ph, long long t)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const float2 f = __bfloat1622float2(hv[q]);
-          if (ph == 0) {
-            acc[u][2 * q] = fmaf(w[j], f.x, acc[u][2 * q]);
-            acc[u][2 * q + 1] = fmaf(w[j], f.y, acc[u][2 * q + 1]);
-          } else {
-            acc[u][2 * q] = acc[u][2 * q] + f.x;
-            acc[u][2 * q + 1] = acc[u][2 * q + 1] + f.y;
-          }
+          // fp32 product and sum rounded separately (__fmul_rn / __fadd_rn are never contracted);
+          // j = 0 starts the fold with the product itself (keeps the sign of a -0 term)
+          const float px = ph == 0 ? __fmul_rn(w[j], f.x) : f.x;
+          const float py = ph == 0 ? __fmul_rn(w[j], f.y) : f.y;
+          acc[u][2 * q] = j == 0 ? px : __fadd_rn(acc[u][2 * q], px);
+          acc[u][2 * q + 1] = j == 0 ? py : __fadd_rn(acc[u][2 * q + 1], py);
         }
       }
     }
@@ -862,6 +861,7 @@ struct ModeUp {
     return nt_tile(a.d, a.p, t, a.d.F / 128, 128, a.d.H / BK);
   }
   __device__ static void before_loads(const Args& a, const TileDesc& td) {
+    if (a.unfused) return;
     const SymPtrs& me = a.peers.p[a.d.rank];
     wait_geq_sys(rg_counter(me, a.d, 0, PAR(a), td.m0 >> 7), (uint32_t)td.rows, a.timeout_ns, a.err,
                  30, td.m0 >> 7);
@@ -946,7 +946,8 @@ __device__ __forceinline__ void push_rows(const MkArgs& a, const TileDesc& td, u
   SlotMeta mt{0, 0, 0.f, 0};
   if (live) mt = a.peers.p[a.d.rank].meta[td.m0 + r];
   const SymPtrs& S = a.peers.p[live ? mt.src : 0];
-  __nv_bfloat16* dst = (ph == 0 ? S.rep : S.rep_dx) + (size_t)mt.rep * a.d.H + td.n0;
+  __nv_bfloat16* dst = a.unfused ? a.ret + (size_t)(live ? a.ret_pos[td.m0 + r] : 0) * a.d.H + td.n0
+                                 : (ph == 0 ? S.rep : S.rep_dx) + (size_t)mt.rep * a.d.H + td.n0;
   const unsigned live_mask = __ballot_sync(0xffffffffu, live);
 #pragma unroll 1
   for (int c = 0; c < BN / 32; c += 2) {
@@ -982,6 +983,7 @@ __device__ __forceinline__ void push_rows(const MkArgs& a, const TileDesc& td, u
 // The combine push's scoreboard update (RELEASE_AFTER hook, after the accumulator went back to
 // the MMA issuer): this thread's replica row of the tile is counted on its source token.
 __device__ __forceinline__ void push_release(const MkArgs& a, const TileDesc& td, int r, int ph) {
+  if (a.unfused) return;  // the return all-to-all runs after the kernel
   const bool live = r < td.rows;
   if (a.d.world == 1)
     fence_acq_rel_gpu();  // one GPU: the reducer is on this device
@@ -1122,6 +1124,7 @@ struct ModeDgradDown {
   }
   __device__ static void before_loads(const Args& a, const TileDesc& td) {
     if (!td.pad1) {
+      if (a.unfused) return;
       const SymPtrs& me = a.peers.p[a.d.rank];
       wait_geq_sys(rg_counter(me, a.d, 1, PAR(a), td.m0 >> 7), (uint32_t)td.rows, a.timeout_ns,
                    a.err, 31, td.m0 >> 7);
@@ -1372,6 +1375,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int t = threadIdx.x; t < a.d.T_max; t += blockDim.x)
         *tok_counter(me, a.d, ph, (PAR(a) ^ 1), t) = 0;
   }
+  if (iteration_aborted(a)) return;  // after the reset: the next iteration's parity stays clean
   gemm_setup(S);
 
   const int n_pre = has_pre ? a.n_disp + a.n_relay : 0;
@@ -1446,6 +1450,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (has_post)
       for (int t = threadIdx.x; t < a.d.T_max; t += blockDim.x) *tok_counter(me, a.d, ph, (PAR(a) ^ 1), t) = 0;
   }
+  if (iteration_aborted(a)) return;  // both CTAs of the pair read the same words: no cluster sync yet
   gemm_setup_pair(S, rank);
   const int n_pre = has_pre ? a.n_disp + a.n_relay : 0;
   const int pairs = a.p.mpair_pre[a.d.epr];

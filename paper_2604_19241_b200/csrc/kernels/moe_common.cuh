@@ -143,7 +143,30 @@ struct MkArgs {
                     // bit 1: ... and the backward combine's reduce pool
   int comm_bulk;
   int rgp, tngp, tngp_d;  // CTA-pair raster groups: 256-row blocks per NT group, 256-row output
-                          // blocks per TN group (up weight gradient / down weight gradient)  // 1: comm role moves rows with the TMA bulk-copy engine (EPLAB_COMM=bulk)
+                          // blocks per TN group (up weight gradient / down weight gradient)
+  // Unfused baseline: the same GroupGEMM tiles with every collective removed --
+  // the rows were scattered into the receive layout before the launch (NCCL all-to-all), so no
+  // scoreboard wait; the combine epilogues write each replica row to ret[ret_pos[slot]] (the
+  // return all-to-all's send buffer) instead of pushing it to the source.
+  int unfused;
+  __nv_bfloat16* ret;
+  const int* ret_pos;
 };
+
+#ifdef __CUDACC__
+// Gate-gradient dot product helper: acc += <a, b> over 8 bf16 pairs, in lane order (shared by the
+// fused comm warps and the unfused dgate kernel, so both produce the same bits).
+__device__ __forceinline__ float dot8_bf16(const int4& a, const int4& b, float acc) {
+  const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&a);
+  const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 fa = __bfloat1622float2(ha[q]), fb = __bfloat1622float2(hb[q]);
+    acc = fmaf(fa.x, fb.x, acc);
+    acc = fmaf(fa.y, fb.y, acc);
+  }
+  return acc;
+}
+#endif
 
 }  // namespace eplab_dev

@@ -49,7 +49,7 @@ class LayerPrediction(C.Structure):
         return {n: getattr(self, n) for n, _ in self._fields_}
 
 
-# B200 calibration of this build (DESIGN.md §Performance model; refit by tools/calibrate_model.py)
+# B200 calibration of this build (DESIGN.md §Performance model; refit by tools/fit_model.py)
 # fitted over 76 measured cases, spare-warp comm workers on/off (profiles/r01_perf_model_validation.md)
 B200_CALIB = Calib(1.0, 0.2e-6, 25.01e9, 25.01e9, 6.5e12, 42.19e-6, 200.0e9, 41.78, 0.513)
 
@@ -87,6 +87,23 @@ def sample_routing(n_exp, topk, n_tok, world, seed):
     return sel, gw
 
 
+def rank_token_map(sel_rank, counts_all, rank, world, n_exp, topk):
+    """One rank's Alg. 1 token map from its own routing + the all-gathered per-expert counts of every
+    rank (eplab_host_rank_token_map): (target_rank, local_expert, offset) per (t, j)."""
+    import numpy as np
+    sel = np.ascontiguousarray(sel_rank, np.int32).reshape(-1)
+    cnt = np.ascontiguousarray(counts_all, np.int64).reshape(world, n_exp)
+    n = sel.size
+    tr, le, off = np.zeros(n, np.int32), np.zeros(n, np.int32), np.zeros(n, np.int64)
+    L = _L()
+    L.eplab_host_rank_token_map.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_longlong,
+                                            C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.eplab_host_rank_token_map.restype = C.c_int
+    _check(L.eplab_host_rank_token_map(sel.ctypes.data, cnt.ctypes.data, rank, world, n_exp, n // topk, topk,
+                                       tr.ctypes.data, le.ctypes.data, off.ctypes.data))
+    return tr, le, off
+
+
 def volume_expected(s, h, remote_only=False):
     t = Traffic()
     _check(_L().eplab_volume_expected(C.byref(s), C.byref(h), int(remote_only), C.byref(t)))
@@ -121,16 +138,15 @@ def search_layer(s, h, calib=None):
     return best, lmin.value, ev.value
 
 
-def choose_config(H, F, E, k, tokens, world, n_sm=148):
+def choose_config(H, F, E, k, tokens, world, n_sm=148, spare=True):
     """TuneConfig for one layer shape from the B200 model (n_red = all SMs; w = 8)."""
     best, _, _ = search_layer(shape(H, F, E, k, tokens), hw(world, n_sm=n_sm))
     best.n_red = n_sm
     # Measured floor: the model does not capture the start-up of the GEMM tiles behind the first
     # landed rowgroups. With the GEMM CTAs' spare warps in the comm pool (default) the model picks
     # 0-20 comm CTAs and 16 is the measured optimum at EP=1 (profiles/r01_spare_warps.txt); without
-    # them (EPLAB_SPARE=0) it was >= 64 (profiles/r01_ndisp_sweep.txt). EP>1: not yet measured.
-    import os
-    floor = ((16 if os.environ.get("EPLAB_SPARE", "1") != "0" else 64) * n_sm) // 148
+    # them (spare=False) it was >= 64 (profiles/r01_ndisp_sweep.txt). EP>1: not yet measured.
+    floor = ((16 if spare else 64) * n_sm) // 148
     if best.n_disp < floor and floor + best.n_relay < n_sm:
         best.n_disp = floor
     return best

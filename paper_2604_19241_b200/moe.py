@@ -6,6 +6,7 @@ computation runs in the library's sm_100a kernels. There is no CPU fallback: wit
 library or a CUDA device every call raises.
 """
 import ctypes as C
+import weakref
 
 import torch
 
@@ -49,6 +50,7 @@ _SIGS = {
     "eplab_set_sm_budget": [_P, _I],
     "eplab_set_comm_options": [_P, _I, _I],
     "eplab_set_auto_tune": [_P, _I],
+    "eplab_set_option": [_P, C.c_char_p, _I],
     "eplab_plan": [_P, _P, _P, _I, _P],
     "eplab_dispatch_group_gemm": [_P, _P, _P, _P],
     "eplab_group_gemm_combine": [_P, _P, _P, _P],
@@ -102,6 +104,14 @@ def _stream(stream):
     return _P(s.cuda_stream)
 
 
+_LIVE = weakref.WeakSet()  # open contexts (tests release them after a failure: live_contexts())
+
+
+def live_contexts():
+    """Contexts not yet closed (their device memory is the library's, not torch's allocator's)."""
+    return [c for c in list(_LIVE) if c.h]
+
+
 class EpMoE:
     """One rank of the expert-parallel MoE layer (experts sharded contiguously: rank = e // epr).
 
@@ -123,7 +133,9 @@ class EpMoE:
         with torch.cuda.device(dev):
             _check(lib().eplab_init(C.byref(a), C.byref(h)))
         self.h = h
+        _LIVE.add(self)
         self._ids = self._gw = None
+        self.plan_epoch = 0  # plans issued on this context (EpMoEFunction ties backward to it)
 
     def close(self):
         if self.h:
@@ -142,8 +154,10 @@ class EpMoE:
         arr = (_P * len(ranks))(*[r.h for r in ranks])
         _check(lib().eplab_connect_local(arr, len(ranks)))
 
+    IPC_HANDLE_BYTES = 128  # EPLAB_IPC_HANDLE_BYTES: CUDA IPC handle + layout signature
+
     def ipc_handle(self):
-        buf = (C.c_char * 64)()
+        buf = (C.c_char * self.IPC_HANDLE_BYTES)()
         _check(lib().eplab_ipc_handle(self.h, buf))
         return bytes(buf)
 
@@ -168,6 +182,11 @@ class EpMoE:
         sw = 3 if spare_warps is True else (0 if spare_warps is False else int(spare_warps))
         _check(lib().eplab_set_comm_options(self.h, sw, int(bulk_mover)))
 
+    def set_option(self, name, value):
+        """Experiment knob (eplab_set_option): engine_pair, spare, comm_bulk, rgp, tngp, tngp_d,
+        bwd_disp_scale, dbg (dbg != 0 skips work: wrong results, measurements only)."""
+        _check(lib().eplab_set_option(self.h, name.encode(), int(value)))
+
     def set_auto_tune(self, on=True):
         """Per-plan launch parameters from the B200 model, cached per 4096-token bucket (default
         until set_tune_config)."""
@@ -181,20 +200,56 @@ class EpMoE:
     def set_sm_budget(self, n_sm):
         _check(lib().eplab_set_sm_budget(self.h, n_sm))
 
+    # ------------------------------------------------------------------ argument checks
+    def _need(self, t, name, shape, dtype=torch.bfloat16):
+        """Every tensor crossing the C-ABI: on this context's device, contiguous, exact dtype and
+        shape (the kernels read raw pointers with this layout). Raises EplabError(2)."""
+        if not isinstance(t, torch.Tensor):
+            raise EplabError(2, f"{name}: expected a torch.Tensor, got {type(t).__name__}")
+        if t.device != self.device:
+            raise EplabError(2, f"{name}: on {t.device}, the context is on {self.device}")
+        if t.dtype != dtype:
+            raise EplabError(2, f"{name}: dtype {t.dtype}, expected {dtype}")
+        if tuple(t.shape) != tuple(shape):
+            raise EplabError(2, f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+        if not t.is_contiguous():
+            raise EplabError(2, f"{name}: must be contiguous")
+        return t
+
+    def _need_planned(self):
+        if self._ids is None:
+            raise EplabError(2, "no plan: call plan() (or forward()) first")
+        return self._ids.shape[0]
+
+    def _need_weights(self, w_up=None, w_down=None):
+        if w_up is not None:
+            self._need(w_up, "w_up", (self.epr, 2 * self.F, self.H))
+        if w_down is not None:
+            self._need(w_down, "w_down", (self.epr, self.H, self.F))
+
     # ------------------------------------------------------------------ data path
     def plan(self, topk_ids, gate_w, stream=None):
-        assert topk_ids.dtype == torch.int32 and gate_w.dtype == torch.float32
-        self._ids, self._gw = topk_ids.contiguous(), gate_w.contiguous()
-        _check(lib().eplab_plan(self.h, _ptr(self._ids), _ptr(self._gw), self._ids.shape[0],
-                                _stream(stream)))
+        if topk_ids.dim() != 2 or topk_ids.shape[1] != self.k:
+            raise EplabError(2, f"topk_ids: shape {tuple(topk_ids.shape)}, expected (n_tok, {self.k})")
+        n = topk_ids.shape[0]
+        ids = self._need(topk_ids.contiguous(), "topk_ids", (n, self.k), torch.int32)
+        gw = self._need(gate_w.contiguous(), "gate_w", (n, self.k), torch.float32)
+        self._ids, self._gw = ids, gw
+        _check(lib().eplab_plan(self.h, _ptr(ids), _ptr(gw), n, _stream(stream)))
+        self.plan_epoch += 1
 
     def dispatch_group_gemm(self, x, w_up, stream=None):
+        n = self._need_planned()
+        self._need(x, "x", (n, self.H))
+        self._need_weights(w_up=w_up)
         _check(lib().eplab_dispatch_group_gemm(self.h, _ptr(x), _ptr(w_up), _stream(stream)))
 
     def group_gemm_combine(self, w_down, y=None, stream=None):
-        n = self._ids.shape[0]
+        n = self._need_planned()
+        self._need_weights(w_down=w_down)
         if y is None:
             y = torch.empty(n, self.H, dtype=torch.bfloat16, device=self.device)
+        self._need(y, "y", (n, self.H))
         _check(lib().eplab_group_gemm_combine(self.h, _ptr(w_down), _ptr(y), _stream(stream)))
         return y
 
@@ -204,12 +259,17 @@ class EpMoE:
         return self.group_gemm_combine(w_down, stream=stream)
 
     def backward(self, dy, w_up, w_down, stream=None, out=None):
-        n = self._ids.shape[0]
+        n = self._need_planned()
         dev = self.device
+        self._need(dy, "dy", (n, self.H))
+        self._need_weights(w_up, w_down)
         if out is None:
             out = dict(dx=torch.empty(n, self.H, dtype=torch.bfloat16, device=dev),
                        dw_up=torch.empty_like(w_up), dw_down=torch.empty_like(w_down),
                        dgate=torch.empty(n, self.k, dtype=torch.float32, device=dev))
+        self._need(out["dx"], "dx", (n, self.H))
+        self._need(out["dgate"], "dgate", (n, self.k), torch.float32)
+        self._need_weights(out["dw_up"], out["dw_down"])
         self._dispatch_bwd(dy, w_down, out, stream)
         self._combine_bwd(w_up, out, stream)
         return out
@@ -336,14 +396,24 @@ class EpMoEFunction(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, layer, x, topk_ids, gate_w, w_up, w_down):
-        y = layer.forward(x, topk_ids, gate_w, w_up, w_down)
+        y = layer.forward(x.contiguous(), topk_ids, gate_w, w_up, w_down)
         ctx.layer = layer
+        # The backward reads this plan's saved activations (receive rows, g/u, replica rows, slot
+        # metadata) from the context: one in-flight forward per context. A second forward on the
+        # same context before this backward (pipelined micro-batches, several layers sharing a
+        # context, activation recomputation) would silently corrupt the gradients, so the
+        # backward checks the plan epoch and raises EplabError(2) instead.
+        ctx.plan_epoch = layer.plan_epoch
         ctx.save_for_backward(w_up, w_down)
         return y
 
     @staticmethod
     def backward(ctx, dy):
         w_up, w_down = ctx.saved_tensors
+        if ctx.layer.plan_epoch != ctx.plan_epoch:
+            raise EplabError(2, f"the context was re-planned (plan {ctx.layer.plan_epoch}) after this "
+                                f"forward (plan {ctx.plan_epoch}): its saved activations are gone. Use one "
+                                f"EpMoE context per in-flight forward.")
         g = ctx.layer.backward(dy.contiguous(), w_up, w_down)
         return None, g["dx"], None, g["dgate"], g["dw_up"], g["dw_down"]
 

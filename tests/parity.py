@@ -1,0 +1,77 @@
+"""Per-element parity measures shared by the GPU tests and tools/ulp_report.py.
+
+An element's error is counted in units in the last place (ulps) of the oracle value in the output's
+format (bf16 for y, dx, dW; fp32 for dgate). Both sides accumulate in fp32, only the summation
+order inside the GEMMs (tensor-core K-blocks vs the oracle's sequential loop) differs, so almost
+every bf16 output is within 1 ulp; the exceptions are rounding-boundary flips and outputs whose
+value is small against the magnitude of their terms (cancellation), which the relative-L2 bound
+and the max-error bound cover.
+"""
+import numpy as np
+
+
+def ulp(r, fp32=False):
+    """ulp of |r| in bf16 (8 significant bits) or fp32 (24); zero / subnormal refs get the ulp of
+    the smallest normal."""
+    a = np.maximum(np.abs(r.astype(np.float64)), np.finfo(np.float32).tiny)
+    e = np.floor(np.log2(a))
+    return np.exp2(e - (23 if fp32 else 7))
+
+
+def ulp_stats(got, ref, fp32=False):
+    g = got.astype(np.float64)
+    r = ref.astype(np.float64)
+    d = np.abs(g - r)
+    n = d / ulp(r, fp32)
+    scale = max(float(np.abs(r).max()), 1e-30)
+    return {
+        "n": int(r.size),
+        "exact": float(np.mean(d == 0)),
+        "le1ulp": float(np.mean(n <= 1.0)),
+        "le2ulp": float(np.mean(n <= 2.0)),
+        "le4ulp": float(np.mean(n <= 4.0)),
+        "max_ulp": float(n.max()) if n.size else 0.0,
+        "max_rel_to_max": float(d.max() / scale) if d.size else 0.0,
+        "rel_l2": float(np.linalg.norm(g - r) / max(np.linalg.norm(r), 1e-30)),
+        "finite": bool(np.isfinite(g).all()),
+    }
+
+
+# Thresholds per kind of output, set from the measured distributions (tools/ulp_report.py,
+# profiles/r02_ulp_report.txt) with margin:
+#   act    y, dx vs the oracle: both pipelines round gu, h, o (and dGU, dX) to bf16, and a 1-ulp flip
+#          of an intermediate o_j moves y by w_j ulp(o_j), which exceeds ulp(y) when the k terms
+#          cancel: measured 99.46-99.95 % within 1 ulp, rel-L2 1.4e-4 - 5e-4
+#   wgrad  dW vs the oracle (one rounding after an fp32 sum over the expert's rows, inputs with the
+#          same intermediate flips): measured 99.93-99.99 % within 1 ulp, rel-L2 0.8e-4 - 1.8e-4
+#   exact_inputs  dW vs an fp32 GEMM of the device's OWN expert buffers: only the fp32 summation
+#          order differs
+#   dgate  fp32 <dY, o>: rel-L2 1e-4 - 2.4e-4 (the o flips above)
+KINDS = {
+    "act": dict(frac_1ulp=0.99, frac_4ulp=0.998, rel_l2=1e-3, max_rel=1e-2),
+    "wgrad": dict(frac_1ulp=0.999, frac_4ulp=0.9995, rel_l2=5e-4, max_rel=1e-2),
+    "exact_inputs": dict(frac_1ulp=0.9999, frac_4ulp=0.99999, rel_l2=1e-4, max_rel=2e-3),
+    "dgate": dict(frac_1ulp=0.0, frac_4ulp=0.0, rel_l2=1e-3, max_rel=5e-3, fp32=True),
+}
+
+
+def assert_ulp(got, ref, name, kind="act"):
+    """The per-element bound of `kind` (KINDS): >= frac_1ulp of the elements within 1 ulp and
+    >= frac_4ulp within 4 ulps of the oracle value, ||got - ref||_2 <= rel_l2 * ||ref||_2, and
+    max |got - ref| <= max_rel * max |ref| (the cancellation tail)."""
+    k = dict(KINDS[kind])
+    fp32 = k.pop("fp32", False)
+    s = ulp_stats(got, ref, fp32)
+    assert s["finite"], f"{name}: non-finite"
+    ok = (s["le1ulp"] >= k["frac_1ulp"] and s["le4ulp"] >= k["frac_4ulp"] and s["rel_l2"] <= k["rel_l2"]
+          and s["max_rel_to_max"] <= k["max_rel"])
+    assert ok, f"{name} ({kind}): {s} vs {k}"
+    return s
+
+
+def assert_layer(got, ref):
+    """Every output of a layer step (dicts of y, dx, dW as bf16 uint16; dgate fp32) vs the oracle."""
+    bf = lambda a: (np.asarray(a).astype(np.uint32) << 16).view(np.float32).reshape(-1)  # noqa: E731
+    for key, kind in (("y", "act"), ("dx", "act"), ("dw_up", "wgrad"), ("dw_down", "wgrad")):
+        assert_ulp(bf(got[key]), bf(ref[key]), key, kind)
+    assert_ulp(np.asarray(got["dgate"]).reshape(-1), np.asarray(ref["dgate"]).reshape(-1), "dgate", "dgate")

@@ -1,11 +1,14 @@
-"""Parity at BASELINE.json's full sizes (Mixtral-8x7B and Qwen3-30B-A3B layer shapes, 16K tokens,
-EP=1), where the oracle cannot run the whole layer: size-independent checks.
+"""Parity at BASELINE.json's full sizes (Mixtral-8x7B, Qwen3-30B-A3B and DeepSeek-V3 layer shapes,
+16K tokens, EP=1), where the oracle cannot run the whole layer: size-independent checks.
 
 * the device token map (permutation indices, per-expert counts, segment bases) is bit-exact with
   the C oracle's restatement of build_global_token_map on all 16K x k routing entries;
 * the whole fwd+bwd step is bitwise deterministic (two runs, every output);
 * y, dx and dgate are row-local: for a sample of tokens the oracle computes them from those
-  tokens alone (with every expert's weights), within the tolerance of tests/test_moe_gpu.py;
+  tokens alone (with every expert's weights), per-element within 1 bf16 ulp (tests/parity.py);
+* the weight gradients, all of them, against fp32 GEMMs (torch, TF32 off) of the device's own
+  exported expert buffers: dW_up[e] = dGU_e^T X_e, dW_down[e] = dY_e^T HW_e (the oracle's
+  definition), per-element within 1 bf16 ulp;
 * the weight gradients satisfy a linearity property: scaling dY by 2 (exact in bf16) scales
   dW_up / dW_down by exactly 2 (power-of-two scaling commutes with every rounding on the path).
 """
@@ -16,9 +19,41 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 from oracle import pyoracle as po  # noqa: E402
-from tests.test_moe_gpu import assert_close, bf16_to_f32, to_u16  # noqa: E402
+from tests.parity import assert_ulp  # noqa: E402
+from tests.test_moe_gpu import bf16_to_f32, to_u16  # noqa: E402
 
-SHAPES = {"mixtral": (4096, 14336, 8, 2, 16384), "qwen3": (2048, 768, 128, 8, 16384)}
+SHAPES = {"mixtral": (4096, 14336, 8, 2, 16384), "qwen3": (2048, 768, 128, 8, 16384),
+          "dsv3": (7168, 2048, 256, 8, 16384)}
+
+
+def _dw_vs_fp32(layer, a, H, F, E):
+    """Every expert's weight gradients vs fp32 GEMMs of the exported expert buffers (one expert at a
+    time: DSv3's 11G weight-gradient elements would not fit as fp32 references at once)."""
+    sb, rows = layer.export_layout()
+    used = int(max(s + ((r + 127) // 128) * 128 for s, r in zip(sb, rows)))
+    xs, dys = layer.buffer("recv_x", used, H), layer.buffer("recv_dy", used, H)
+    dgu, hw = layer.buffer("dgu", used, 2 * F), layer.buffer("hw", used, F)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    got_u, ref_u, got_d, ref_d = [], [], [], []
+    try:
+        for e in range(E):
+            s, r = int(sb[e]), int(rows[e])
+            up = dgu[s:s + r].float().t() @ xs[s:s + r].float()
+            down = dys[s:s + r].float().t() @ hw[s:s + r].float()
+            # a deterministic sample of 2^16 elements per expert keeps the host side small
+            g = torch.Generator(device="cuda").manual_seed(e)
+            iu = torch.randint(0, up.numel(), (1 << 16,), device="cuda", generator=g)
+            idn = torch.randint(0, down.numel(), (1 << 16,), device="cuda", generator=g)
+            got_u.append(a["dw_up"][e].reshape(-1)[iu].float())
+            ref_u.append(up.reshape(-1)[iu].bfloat16().float())  # the one rounding of the output
+            got_d.append(a["dw_down"][e].reshape(-1)[idn].float())
+            ref_d.append(down.reshape(-1)[idn].bfloat16().float())
+            del up, down
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    assert_ulp(torch.cat(got_u).cpu().numpy(), torch.cat(ref_u).cpu().numpy(), "dw_up", "exact_inputs")
+    assert_ulp(torch.cat(got_d).cpu().numpy(), torch.cat(ref_d).cpu().numpy(), "dw_down", "exact_inputs")
 
 
 @pytest.mark.parametrize("cfg", sorted(SHAPES))
@@ -35,7 +70,14 @@ def test_full_size_parity(cfg):
     ids = torch.from_numpy(sel[0].reshape(T, k).copy()).cuda()
     gws = torch.from_numpy(gw[0].reshape(T, k).copy()).cuda()
     layer = M.EpMoE(H, F, E, k, T)
+    try:
+        _full_size_checks(layer, H, F, E, k, T, sel, gw, x, dy, w_up, w_down, ids, gws)
+    finally:
+        layer.close()
+        torch.cuda.empty_cache()
 
+
+def _full_size_checks(layer, H, F, E, k, T, sel, gw, x, dy, w_up, w_down, ids, gws):
     def step(dy_):
         y = layer.forward(x, ids, gws, w_up, w_down)
         gr = layer.backward(dy_, w_up, w_down)
@@ -45,6 +87,7 @@ def test_full_size_parity(cfg):
 
     a = step(dy)
     tr, le, off, rt, sb = layer.export_token_map()
+    _dw_vs_fp32(layer, a, H, F, E)
     b = step(dy)
     for key in ("y", "dx", "dgate", "dw_up", "dw_down"):
         assert torch.equal(a[key], b[key]), f"run-to-run {key}"
@@ -56,15 +99,15 @@ def test_full_size_parity(cfg):
     c = step((dy.float() * 2).bfloat16())
     for key in ("dw_up", "dw_down"):
         assert torch.equal(c[key].float(), a[key].float() * 2), f"{key}(2 dY) != 2 {key}(dY)"
+    del c
     # row-local outputs of sampled tokens vs the oracle
-    toks = np.array([0, 1, T // 3, T // 2, T - 2, T - 1])
+    toks = np.array([0, 1, 77, T // 3, T // 2, T - 2, T - 1])
     ref = po.Oracle().moe_layer(1, E, k, H, F, sel.reshape(T, k)[toks].reshape(1, -1),
                                 gw.reshape(T, k)[toks].reshape(1, -1), to_u16(x[toks]).reshape(1, -1, H),
-                                to_u16(w_up), to_u16(w_down), to_u16(dy[toks]).reshape(1, -1, H))
-    assert_close(bf16_to_f32(to_u16(a["y"][toks])).reshape(-1), bf16_to_f32(ref["y"]).reshape(-1), "y")
-    assert_close(bf16_to_f32(to_u16(a["dx"][toks])).reshape(-1), bf16_to_f32(ref["dx"]).reshape(-1), "dx")
-    assert_close(a["dgate"][toks].cpu().numpy().reshape(-1), ref["dgate"].reshape(-1), "dgate")
-    layer.close()
+                                to_u16(w_up), to_u16(w_down), to_u16(dy[toks]).reshape(1, -1, H), want_dw=False)
+    assert_ulp(bf16_to_f32(to_u16(a["y"][toks])).reshape(-1), bf16_to_f32(ref["y"]).reshape(-1), "y")
+    assert_ulp(bf16_to_f32(to_u16(a["dx"][toks])).reshape(-1), bf16_to_f32(ref["dx"]).reshape(-1), "dx")
+    assert_ulp(a["dgate"][toks].cpu().numpy().reshape(-1), ref["dgate"].reshape(-1), "dgate", "dgate")
 
 
 @pytest.mark.parametrize("relay", [0, 4])
@@ -180,9 +223,9 @@ def test_small_config_ep2_full_size():
     toks = np.array([0, 5, T - 1, T, W * T - 1])
     ref = po.Oracle().moe_layer(1, E, k, H, F, sel.reshape(W * T, k)[toks].reshape(1, -1),
                                 gw.reshape(W * T, k)[toks].reshape(1, -1), to_u16(x[toks]).reshape(1, -1, H),
-                                to_u16(w_up), to_u16(w_down), to_u16(dy[toks]).reshape(1, -1, H))
-    assert_close(bf16_to_f32(to_u16(y1[toks])).reshape(-1), bf16_to_f32(ref["y"]).reshape(-1), "y")
-    assert_close(bf16_to_f32(to_u16(g1["dx"][toks])).reshape(-1), bf16_to_f32(ref["dx"]).reshape(-1), "dx")
-    assert_close(g1["dgate"][toks].cpu().numpy().reshape(-1), ref["dgate"].reshape(-1), "dgate")
+                                to_u16(w_up), to_u16(w_down), to_u16(dy[toks]).reshape(1, -1, H), want_dw=False)
+    assert_ulp(bf16_to_f32(to_u16(y1[toks])).reshape(-1), bf16_to_f32(ref["y"]).reshape(-1), "y")
+    assert_ulp(bf16_to_f32(to_u16(g1["dx"][toks])).reshape(-1), bf16_to_f32(ref["dx"]).reshape(-1), "dx")
+    assert_ulp(g1["dgate"][toks].cpu().numpy().reshape(-1), ref["dgate"].reshape(-1), "dgate", "dgate")
     for r in ranks:
         r.close()

@@ -2,8 +2,10 @@
 outputs for the integer addressing), through the C-ABI of libeplab_b200.so.
 
 Tolerances (bf16 outputs, fp32 accumulation everywhere, different summation order inside the
-tensor-core GEMMs): max|gpu - oracle| <= 2e-2 * max|oracle| and
-||gpu - oracle||_2 <= 1e-2 * ||oracle||_2 (about two bf16 ulps). Integer outputs: bit-exact.
+tensor-core GEMMs): the per-element bounds of tests/parity.py -- >= 99 % of y / dx and >= 99.9 % of
+dW elements within 1 bf16 ulp of the oracle, relative L2 <= 1e-3 (5e-4 for dW). Integer outputs:
+bit-exact. assert_close (2e-2 max / 1e-2 L2) remains only for the opt-in non-bitwise split-batch
+variant, whose weight gradients carry an extra bf16 rounding by design.
 """
 import os
 
@@ -62,9 +64,10 @@ class Problem:
                                      self.w_up, self.w_down, self.dy)
 
 
-def run_layer(prob, world=None, cfg=None, reps=1, comm=None):
+def run_layer(prob, world=None, cfg=None, reps=1, comm=None, keep=()):
     """Runs fwd+bwd on `world` virtual ranks sharing cuda:0 (each with its own SM budget and
-    stream). Returns per-rank outputs as numpy (bf16 as uint16)."""
+    stream). Returns per-rank outputs as numpy (bf16 as uint16); `keep` names internal buffers
+    ("rep", "rep_dx": the [T*k][H] replica slots at the source) copied into the last rep's outputs."""
     m = moe()
     W = world or prob.world
     assert prob.world * prob.T % W == 0
@@ -115,7 +118,9 @@ def run_layer(prob, world=None, cfg=None, reps=1, comm=None):
             ranks[r].check(streams[r])
         torch.cuda.synchronize()
         outs.append([dict(y=to_u16(ys[r]), dx=to_u16(gs[r]["dx"]), dgate=gs[r]["dgate"].cpu().numpy(),
-                          dw_up=to_u16(gs[r]["dw_up"]), dw_down=to_u16(gs[r]["dw_down"])) for r in range(W)])
+                          dw_up=to_u16(gs[r]["dw_up"]), dw_down=to_u16(gs[r]["dw_down"]),
+                          **{b: to_u16(ranks[r].buffer(b, T * prob.k, prob.H)) for b in keep})
+                     for r in range(W)])
     maps = [rk.export_token_map() for rk in ranks]
     sched = [rk.export_schedule() for rk in ranks]
     for rk in ranks:
@@ -132,12 +137,10 @@ def gather(out):
 
 
 def check_vs_oracle(prob, got):
-    ref = prob.oracle()
-    assert_close(bf16_to_f32(got["y"]).reshape(-1), bf16_to_f32(ref["y"]).reshape(-1), "y")
-    assert_close(bf16_to_f32(got["dx"]).reshape(-1), bf16_to_f32(ref["dx"]).reshape(-1), "dx")
-    assert_close(got["dgate"].reshape(-1), ref["dgate"].reshape(-1), "dgate")
-    assert_close(bf16_to_f32(got["dw_up"]).reshape(-1), bf16_to_f32(ref["dw_up"]).reshape(-1), "dw_up")
-    assert_close(bf16_to_f32(got["dw_down"]).reshape(-1), bf16_to_f32(ref["dw_down"]).reshape(-1), "dw_down")
+    """Per-element bounds of tests/parity.py (>= 99 % of y / dx and >= 99.9 % of dW within 1 bf16
+    ulp of the oracle, relative L2 <= 1e-3 / 5e-4)."""
+    from tests.parity import assert_layer
+    assert_layer(got, prob.oracle())
 
 
 @pytest.mark.parametrize("E,k,T", [(8, 2, 384), (16, 4, 200)])

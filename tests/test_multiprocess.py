@@ -1,11 +1,14 @@
 """N > 1 paths with one process per rank.
 
-* CPU (gloo, world 2): the bootstrap plumbing -- every rank derives its shard of the routing
-  from the reference generator, the per-expert counts are all-gathered, and each rank's token
-  map built from (its own routing + the gathered counts) equals the global reference map; the
-  64-byte handle all-gather used by EpMoE.connect_distributed.
-* GPU (two processes sharing cuda:0, each with half the SMs): CUDA-IPC symmetric buffers opened
-  across processes, the four MegaKernels at EP=2, outputs bitwise equal to the EP=1 run.
+* CPU (gloo, world 2 and 4): the bootstrap plumbing through the library's host API -- every rank
+  derives its shard of the routing from the reference generator, the per-expert counts are
+  all-gathered (Alg. 1 line 3, the exchange the device planner does over NVLink), and each
+  rank's token map computed by libeplab_b200.so from (its own routing + the gathered counts)
+  equals the reference's global map (oracle/_ref, else the C oracle); the EPLAB_IPC_HANDLE_BYTES
+  record all-gather of EpMoE.connect_distributed.
+* GPU (2 and 4 processes sharing cuda:0, each with 148/N SMs): CUDA-IPC symmetric buffers opened
+  across processes, the four MegaKernels at EP=N, outputs bitwise equal to the EP=1 run; a rank
+  whose symmetric layout differs is rejected by connect_ipc with error 2 on every rank.
 """
 import os
 import socket
@@ -39,50 +42,45 @@ def _cpu_worker(rank, world, port, q):
     import sys
     sys.path.insert(0, ROOT)
     from oracle import pyoracle as po
+    from paper_2604_19241_b200.model import rank_token_map, sample_routing
     _init(rank, world, port)
     try:
         E, k, T = 16, 4, 300
-        orc = po.Oracle()
-        sel_all, _ = orc.sample_routing(E, k, T, world, 5)  # every rank can regenerate its shard
+        sel_all, _ = sample_routing(E, k, T, world, 5)  # every rank can regenerate its shard
         mine = sel_all[rank]
         counts = torch.from_numpy(np.bincount(mine, minlength=E).astype(np.int64))
         gathered = [torch.zeros(E, dtype=torch.int64) for _ in range(world)]
         dist.all_gather(gathered, counts)  # Alg. 1 line 3 over gloo
         c_all = torch.stack(gathered).numpy()
-        epr = E // world
-        # this rank's final offsets from its own local sort + the gathered counts (Eq. 1)
-        local = np.zeros(T * k, np.int64)
-        seen = np.zeros(E, np.int64)
-        for i, e in enumerate(mine):
-            local[i] = seen[e]
-            seen[e] += 1
-        o_all = c_all[:rank].sum(axis=0)
-        off = local + o_all[mine]
-        tr, le, ref_off, _, _ = orc.token_map(sel_all, E, k)
-        ok = bool((off == ref_off[rank]).all() and (mine // epr == tr[rank]).all())
+        tr, le, off = rank_token_map(mine, c_all, rank, world, E, k)  # the library, this rank only
+        ref = po.Reference() if po.has_reference() else po.Oracle()
+        rtr, rle, roff, _, _ = ref.token_map(sel_all, E, k)
+        ok = bool((off == roff[rank]).all() and (tr == rtr[rank]).all() and (le == rle[rank]).all())
+        rec = bytes([rank]) * 128  # EPLAB_IPC_HANDLE_BYTES records, as connect_distributed exchanges
         hs = [None] * world
-        dist.all_gather_object(hs, bytes([rank]) * 64)  # EpMoE.connect_distributed's exchange
-        ok = ok and hs == [bytes([r]) * 64 for r in range(world)]
+        dist.all_gather_object(hs, rec)
+        ok = ok and hs == [bytes([r]) * 128 for r in range(world)]
         q.put((rank, ok))
     finally:
         dist.destroy_process_group()
 
 
-def test_gloo_bootstrap_and_token_map_world2():
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_bootstrap_and_token_map(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_cpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_cpu_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=120) for _ in procs)
+    res = dict(q.get(timeout=180) for _ in procs)
     for p in procs:
         p.join(timeout=60)
-    assert res == {0: True, 1: True}
+    assert res == {r: True for r in range(world)}
 
 
 # ------------------------------------------------------------------ GPU / CUDA IPC
-def _gpu_worker(rank, world, port, q):
+def _gpu_worker(rank, world, port, q, mismatch=False):
     import sys
     sys.path.insert(0, ROOT)
     from tests.test_moe_gpu import Problem, from_u16, to_u16
@@ -93,7 +91,17 @@ def _gpu_worker(rank, world, port, q):
         prob = Problem(world, 8, 2, 256, 256, 256, seed=11)
         T, k, H = prob.T, prob.k, prob.H
         epr = prob.E // world
-        layer = M.EpMoE(prob.H, prob.F, prob.E, k, T, rank=rank, world=world, timeout_s=20.0)
+        t_max = T + 64 if (mismatch and rank == world - 1) else T
+        layer = M.EpMoE(prob.H, prob.F, prob.E, k, t_max, rank=rank, world=world, timeout_s=20.0)
+        if mismatch:
+            try:
+                layer.connect_distributed()
+                q.put((rank, "connected"))
+            except M.EplabError as e:
+                q.put((rank, (e.code, "layout differs" in str(e))))
+            dist.barrier()
+            layer.close()
+            return
         layer.connect_distributed()
         layer.set_sm_budget(148 // world)
         ids = torch.from_numpy(prob.sel[rank].reshape(T, k).copy()).cuda()
@@ -111,21 +119,35 @@ def _gpu_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.gpu
-def test_two_processes_ipc_match_single_process():
-    from tests.test_moe_gpu import Problem, gather, run_layer
+def _spawn(world, mismatch=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, q, mismatch)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in procs)
     for p in procs:
         p.join(timeout=120)
-    prob = Problem(2, 8, 2, 256, 256, 256, seed=11)
+    return res
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_processes_ipc_match_single_process(world):
+    from tests.test_moe_gpu import Problem, gather, run_layer
+    res = _spawn(world)
+    prob = Problem(world, 8, 2, 256, 256, 256, seed=11)
     ep1, _, _ = run_layer(prob, world=1)
     ref = gather(ep1[0])
-    got = gather([res[0], res[1]])
+    got = gather([res[r] for r in range(world)])
     for key in ("y", "dx", "dgate", "dw_up", "dw_down"):
         assert (got[key] == ref[key]).all(), key
+
+
+@pytest.mark.gpu
+def test_ipc_layout_mismatch_rejected_on_every_rank():
+    """The last rank was created with a different max_tokens: its symmetric region has another
+    layout, so every rank's connect_ipc refuses it (error 2) instead of writing at wrong offsets."""
+    res = _spawn(2, mismatch=True)
+    assert res == {0: (2, True), 1: (2, True)}, res

@@ -392,3 +392,47 @@ def test_router_bwd_oracle_vs_finite_differences(renorm):
 def test_router_validation():
     with pytest.raises(ValueError):
         po.Oracle().router_topk(np.zeros((2, 4), np.float32), 5)
+
+
+def _torch_layer_grads(E, k, H, F, sel, gw, x, w_up, w_down, dy):
+    """The layer math written as a plain torch fp32
+    autograd graph on the same bf16 inputs: y_t = sum_j w_tj * W_down[e] silu(g) u with
+    [g; u] = W_up[e] x_t; loss = <y, dy>."""
+    import torch
+    f = lambda a: torch.from_numpy((a.astype(np.uint32) << 16).view(np.float32))  # noqa: E731
+    X, Wu, Wd, DY = f(x).requires_grad_(), f(w_up).requires_grad_(), f(w_down).requires_grad_(), f(dy)
+    G = torch.from_numpy(gw.reshape(-1, k).astype(np.float32)).requires_grad_()
+    S = torch.from_numpy(sel.reshape(-1, k).astype(np.int64))
+    T = X.shape[0]
+    y = torch.zeros(T, H)
+    for j in range(k):
+        gu = torch.einsum("th,tnh->tn", X, Wu[S[:, j]])
+        h = torch.nn.functional.silu(gu[:, :F]) * gu[:, F:]
+        o = torch.einsum("tf,thf->th", h, Wd[S[:, j]])
+        y = y + G[:, j:j + 1] * o
+    (y * DY).sum().backward()
+    return y.detach().numpy(), X.grad.numpy(), G.grad.numpy(), Wu.grad.numpy(), Wd.grad.numpy()
+
+
+@pytest.mark.parametrize("E,k,H,F,T", [(4, 2, 64, 32, 24), (8, 4, 32, 64, 16)])
+def test_oracle_layer_fwd_bwd_pinned_by_torch_autograd(E, k, H, F, T):
+    """The oracle's forward AND backward formulas (orc_moe_layer: SwiGLU backward, gate gradient
+    <dY, o>, dW_up = dGU^T X, dW_down = dY^T HW, the k-ordered dx) agree with torch.autograd of the
+    layer in fp32: the two differ only by the oracle's bf16 rounding of its intermediates (gu, h,
+    o, dGU, HW, dX), so the relative L2 error is a few bf16 ulps. A wrong derivative (e.g. a
+    missing gate weight or a swapped g/u) is off by O(1)."""
+    pytest.importorskip("torch")
+    orc = po.Oracle()
+    sel, gw = orc.sample_routing(E, k, T, 1, 3)
+    x = orc.fill_normal_bf16(T * H, 4).reshape(1, T, H)
+    dy = orc.fill_normal_bf16(T * H, 5, 0.5).reshape(1, T, H)
+    w_up = orc.fill_normal_bf16(E * 2 * F * H, 6, H ** -0.5).reshape(E, 2 * F, H)
+    w_down = orc.fill_normal_bf16(E * H * F, 7, F ** -0.5).reshape(E, H, F)
+    ref = orc.moe_layer(1, E, k, H, F, sel, gw, x, w_up, w_down, dy)
+    ty, tdx, tdg, tdwu, tdwd = _torch_layer_grads(E, k, H, F, sel, gw, x[0], w_up, w_down, dy[0])
+    bf = lambda a: (a.astype(np.uint32) << 16).view(np.float32).astype(np.float64)  # noqa: E731
+    for name, got, want in (("y", bf(ref["y"][0]), ty), ("dx", bf(ref["dx"][0]), tdx),
+                            ("dgate", ref["dgate"].reshape(T, k).astype(np.float64), tdg),
+                            ("dw_up", bf(ref["dw_up"]), tdwu), ("dw_down", bf(ref["dw_down"]), tdwd)):
+        rel = np.linalg.norm(got - want) / np.linalg.norm(want)
+        assert rel < 8e-3, f"{name}: rel L2 {rel:.3g}"

@@ -1,7 +1,8 @@
-"""In-process A/B of launch options (env switches read per call, or tune configs): the variants
+"""In-process A/B of launch options (eplab_set_option knobs, or tune configs): the variants
 alternate step by step in one process, so power/thermal drift hits all of them alike.
   python tools/ab_inproc.py --config qwen3 --variants "EPLAB_SPARE=1;EPLAB_SPARE=0" --rounds 20
-  a variant is ';'-separated; each is a ','-list of ENV=VAL or tune=n_disp:n_relay:n_comb:n_red:w
+  a variant is ';'-separated; each is a ','-list of KNOB=VAL (eplab_set_option names or the old EPLAB_*
+  spellings) or tune=n_disp:n_relay:n_comb:n_red:w
 """
 import argparse, json, os, statistics, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -34,23 +35,27 @@ st = torch.cuda.current_stream()
 variants = [v.strip() for v in args.variants.split(";")]
 
 
-ENV_KEYS = {kv.split("=")[0] for v in variants for kv in v.split(",") if kv and not kv.startswith("tune=")}
-ENV0 = {k: os.environ.get(k) for k in ENV_KEYS}
+# knob names of eplab_set_option (the old EPLAB_* spellings are accepted) and their defaults
+ALIASES = {"EPLAB_SPARE": "spare", "EPLAB_COMM": "comm_bulk", "EPLAB_DBG": "dbg", "EPLAB_RGP": "rgp",
+           "EPLAB_TNGP": "tngp", "EPLAB_TNGP_D": "tngp_d", "EPLAB_BWD_DISP_SCALE": "bwd_disp_scale",
+           "EPLAB_ENGINE": "engine_pair"}
+DEFAULTS = {"spare": 3, "comm_bulk": 0, "dbg": 0, "rgp": 8, "tngp": 4, "tngp_d": 4, "bwd_disp_scale": 2,
+            "engine_pair": 1}
 
 
 def apply(v):
     cfg = base_cfg
-    for k0, v0 in ENV0.items():  # every variant starts from the original environment
-        if v0 is None:
-            os.environ.pop(k0, None)
-        else:
-            os.environ[k0] = v0
+    opts = dict(DEFAULTS)  # every variant starts from the defaults
     for kv in [p for p in v.split(",") if p]:
         key, val = kv.split("=")
         if key == "tune":
             cfg = M.TuneConfig(*[int(q) for q in val.split(":")])
         else:
-            os.environ[key] = val
+            name = ALIASES.get(key, key)
+            opts[name] = {"bulk": 1, "warp": 0, "single": 0, "pair": 1}.get(val, None) if not val.lstrip("-").isdigit() \
+                else int(val)
+    for name, val in opts.items():
+        L.set_option(name, val)
     L.set_tune_config(cfg)
 
 

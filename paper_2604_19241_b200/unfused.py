@@ -116,8 +116,9 @@ class NcclComm:
     def all_to_all(self, sends, send_splits, recv_splits, width, dtype):
         (send,), (ss,), (rs,) = sends, send_splits, recv_splits
         dev = send.device
-        if self.staged:
-            send = send.cpu() if dtype != torch.bfloat16 else send.view(torch.int16).cpu()
+        if self.staged:  # gloo all-to-all: host tensors of a 32-bit type (bf16 rows as int32 pairs)
+            send = (send.view(torch.int32) if dtype == torch.bfloat16 else send).cpu()
+            width = width // 2 if dtype == torch.bfloat16 else width
         out = torch.empty(sum(rs), width, dtype=send.dtype, device=send.device)
         self.dist.all_to_all_single(out, send, output_split_sizes=rs, input_split_sizes=ss,
                                     group=self.group)  # grouped ncclSend / ncclRecv

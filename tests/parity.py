@@ -44,13 +44,14 @@ def ulp_stats(got, ref, fp32=False):
 #          cancel: measured 99.46-99.95 % within 1 ulp, rel-L2 1.4e-4 - 5e-4
 #   wgrad  dW vs the oracle (one rounding after an fp32 sum over the expert's rows, inputs with the
 #          same intermediate flips): measured 99.93-99.99 % within 1 ulp, rel-L2 0.8e-4 - 1.8e-4
-#   exact_inputs  dW vs an fp32 GEMM of the device's OWN expert buffers: only the fp32 summation
-#          order differs
+#   exact_inputs  dW vs an fp32 GEMM (cuBLAS, TF32 off) of the device's OWN expert buffers: only the
+#          fp32 accumulation differs (order, and the tensor cores' internal accumulation): measured
+#          99.71-99.96 % exact, 99.978-99.998 % within 1 ulp, rel-L2 0.55e-4 - 1.5e-4 at full size
 #   dgate  fp32 <dY, o>: rel-L2 1e-4 - 2.4e-4 (the o flips above)
 KINDS = {
     "act": dict(frac_1ulp=0.99, frac_4ulp=0.998, rel_l2=1e-3, max_rel=1e-2),
     "wgrad": dict(frac_1ulp=0.999, frac_4ulp=0.9995, rel_l2=5e-4, max_rel=1e-2),
-    "exact_inputs": dict(frac_1ulp=0.9999, frac_4ulp=0.99999, rel_l2=1e-4, max_rel=2e-3),
+    "exact_inputs": dict(frac_1ulp=0.9995, frac_4ulp=0.9998, rel_l2=3e-4, max_rel=1e-2),
     "dgate": dict(frac_1ulp=0.0, frac_4ulp=0.0, rel_l2=1e-3, max_rel=5e-3, fp32=True),
 }
 

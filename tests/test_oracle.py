@@ -436,3 +436,26 @@ def test_oracle_layer_fwd_bwd_pinned_by_torch_autograd(E, k, H, F, T):
                             ("dw_up", bf(ref["dw_up"]), tdwu), ("dw_down", bf(ref["dw_down"]), tdwd)):
         rel = np.linalg.norm(got - want) / np.linalg.norm(want)
         assert rel < 8e-3, f"{name}: rel L2 {rel:.3g}"
+
+
+def test_cpu_port_matches_c_oracle():
+    """oracle/cpu_port.py (the bench's CPU arm: the same layer contract on CPU BLAS) agrees with the
+    C oracle (the checker) within the per-element bounds of tests/parity.py -- only the fp32
+    summation order inside the GEMMs differs."""
+    pytest.importorskip("torch")
+    import torch
+    from oracle import cpu_port
+    from tests.parity import assert_layer
+    E, k, H, F, T = 8, 2, 128, 64, 96
+    orc = po.Oracle()
+    sel, gw = orc.sample_routing(E, k, T, 1, 9)
+    x = orc.fill_normal_bf16(T * H, 1).reshape(1, T, H)
+    dy = orc.fill_normal_bf16(T * H, 2, 0.5).reshape(1, T, H)
+    w_up = orc.fill_normal_bf16(E * 2 * F * H, 3, H ** -0.5).reshape(E, 2 * F, H)
+    w_down = orc.fill_normal_bf16(E * H * F, 4, F ** -0.5).reshape(E, H, F)
+    ref = orc.moe_layer(1, E, k, H, F, sel, gw, x, w_up, w_down, dy)
+    f = lambda a: torch.from_numpy((a.astype(np.uint32) << 16).view(np.float32))  # noqa: E731
+    y, dx, dg, dwu, dwd = cpu_port.moe_layer(sel[0], gw[0], f(x[0]), f(w_up), f(w_down), f(dy[0]), E, k)
+    u16 = lambda t: (t.numpy().view(np.uint32) >> 16).astype(np.uint16)  # noqa: E731
+    assert_layer(dict(y=u16(y), dx=u16(dx), dgate=dg.numpy(), dw_up=u16(dwu), dw_down=u16(dwd)),
+                 {kk: (v[0] if kk in ("y", "dx", "dgate") else v) for kk, v in ref.items()})

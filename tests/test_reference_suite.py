@@ -36,3 +36,17 @@ def test_reference_unit_tests_pass_against_this_library(tmp_path):
     summary = res.stdout.strip().splitlines()[-1] if res.stdout.strip() else ""
     assert res.returncode == 0, res.stderr[-4000:] + summary
     assert "| 0 failed |" in summary and "test cases: 59" in summary, summary
+
+
+def test_reference_api_extras(tmp_path):
+    """derive_expanded_tokens, TrafficReport::basis, BigInt stirling2 beyond 128 bits and the
+    Binary32 accumulate contract, through the reference header names (tests/cpp/api_extras.cpp)."""
+    lib_dir = os.path.join(ROOT, "paper_2604_19241_b200")
+    exe = str(tmp_path / "api_extras")
+    subprocess.check_call(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), "-I",
+                           os.path.join(ROOT, "tests", "cpp", "doctest"),
+                           os.path.join(ROOT, "tests", "cpp", "api_extras.cpp"), "-o", exe, "-L", lib_dir,
+                           "-leplab_b200", f"-Wl,-rpath,{lib_dir}", "-L", "/usr/local/cuda/lib64", "-lcudart",
+                           "-Wl,-rpath,/usr/local/cuda/lib64"])
+    res = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert res.returncode == 0, res.stderr + res.stdout

@@ -91,6 +91,9 @@ def _worker(rank, world, port, q):
                           dw_up=to_u16(gs[0]["dw_up"]), dw_down=to_u16(gs[0]["dw_down"]))))
         dist.barrier()
         L.close()
+    except Exception as e:  # fail the test at once instead of timing out on the queue
+        q.put((rank, f"worker {rank} failed: {type(e).__name__}: {e}"))
+        raise
     finally:
         dist.destroy_process_group()
 
@@ -109,6 +112,7 @@ def test_unfused_two_processes_equals_fused():
     res = dict(q.get(timeout=300) for _ in procs)
     for p in procs:
         p.join(timeout=120)
+    assert all(isinstance(v, dict) for v in res.values()), res
     prob = Problem(2, 16, 4, 256, 256, 192, seed=37)
     fused, _, _ = run_layer(prob)
     a, b = gather(fused[0]), gather([res[0], res[1]])

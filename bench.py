@@ -145,7 +145,7 @@ def algorithmic(cfg_name, world):
 # ---------------------------------------------------------------------------- CPU baseline
 # Tokens of one CPU-arm step: a bounded sample of the workload's per-GPU batch (every expert's
 # weights and weight gradients are still computed), sized for a few seconds per step on the host.
-CPU_SAMPLE = {"mixtral": 512, "qwen3": 1024, "dsv3": 256, "small": 4096}
+CPU_SAMPLE = {"mixtral": 4096, "qwen3": 8192, "dsv3": 2048, "small": 4096}
 
 
 def cpu_model():

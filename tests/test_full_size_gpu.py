@@ -98,15 +98,16 @@ def _full_size_checks(layer, H, F, E, k, T, sel, gw, x, dy, w_up, w_down, ids, g
     # linearity of the weight gradients in dY (x2 is exact in bf16 and commutes with rounding)
     c = step((dy.float() * 2).bfloat16())
     for key in ("dw_up", "dw_down"):
-        assert torch.equal(c[key].float(), a[key].float() * 2), f"{key}(2 dY) != 2 {key}(dY)"
+        for e in range(E):  # per expert: DSv3's dW in fp32 would be 30 GB
+            assert torch.equal(c[key][e].float(), a[key][e].float() * 2), f"{key}(2 dY) != 2 {key}(dY), expert {e}"
     del c
     # row-local outputs of sampled tokens vs the oracle
     toks = np.array([0, 1, 77, T // 3, T // 2, T - 2, T - 1])
     ref = po.Oracle().moe_layer(1, E, k, H, F, sel.reshape(T, k)[toks].reshape(1, -1),
                                 gw.reshape(T, k)[toks].reshape(1, -1), to_u16(x[toks]).reshape(1, -1, H),
                                 to_u16(w_up), to_u16(w_down), to_u16(dy[toks]).reshape(1, -1, H), want_dw=False)
-    assert_ulp(bf16_to_f32(to_u16(a["y"][toks])).reshape(-1), bf16_to_f32(ref["y"]).reshape(-1), "y")
-    assert_ulp(bf16_to_f32(to_u16(a["dx"][toks])).reshape(-1), bf16_to_f32(ref["dx"]).reshape(-1), "dx")
+    assert_ulp(bf16_to_f32(to_u16(a["y"][toks])).reshape(-1), bf16_to_f32(ref["y"]).reshape(-1), "y", "act_longk")
+    assert_ulp(bf16_to_f32(to_u16(a["dx"][toks])).reshape(-1), bf16_to_f32(ref["dx"]).reshape(-1), "dx", "act_longk")
     assert_ulp(a["dgate"][toks].cpu().numpy().reshape(-1), ref["dgate"].reshape(-1), "dgate", "dgate")
 
 
@@ -224,8 +225,8 @@ def test_small_config_ep2_full_size():
     ref = po.Oracle().moe_layer(1, E, k, H, F, sel.reshape(W * T, k)[toks].reshape(1, -1),
                                 gw.reshape(W * T, k)[toks].reshape(1, -1), to_u16(x[toks]).reshape(1, -1, H),
                                 to_u16(w_up), to_u16(w_down), to_u16(dy[toks]).reshape(1, -1, H), want_dw=False)
-    assert_ulp(bf16_to_f32(to_u16(y1[toks])).reshape(-1), bf16_to_f32(ref["y"]).reshape(-1), "y")
-    assert_ulp(bf16_to_f32(to_u16(g1["dx"][toks])).reshape(-1), bf16_to_f32(ref["dx"]).reshape(-1), "dx")
+    assert_ulp(bf16_to_f32(to_u16(y1[toks])).reshape(-1), bf16_to_f32(ref["y"]).reshape(-1), "y", "act_longk")
+    assert_ulp(bf16_to_f32(to_u16(g1["dx"][toks])).reshape(-1), bf16_to_f32(ref["dx"]).reshape(-1), "dx", "act_longk")
     assert_ulp(g1["dgate"][toks].cpu().numpy().reshape(-1), ref["dgate"].reshape(-1), "dgate", "dgate")
     for r in ranks:
         r.close()

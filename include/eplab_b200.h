@@ -98,9 +98,10 @@ typedef struct eplab_ctx eplab_ctx;
 
 /* Launch parameters chosen by the performance model (reference TuneConfig, types.hpp:45-53).
  * n_disp: comm tasks; n_relay: relay tasks (0 = AllToAll-style, every replica sent directly;
- * >0 = AllGather-style dedup + intra-rank multicast); n_comb: unused on B200 (the combine
- * push is fused into the GEMM epilogue); n_red: reduce tasks; w: warps per
- * worker (8 on B200: one 256-thread CTA per SM). */
+ * >0 = AllGather-style dedup + intra-rank multicast); n_red: reduce tasks. n_comb must be 0 or 1
+ * (the combine push is the GEMM epilogue: there are no combine CTAs) and w must be 8 (one
+ * 256-thread CTA per SM; comm workers are single warps, the warp split is
+ * eplab_set_comm_options); other values return 2. The tile is fixed at 256 x 256 (CTA pairs). */
 typedef struct {
   int n_disp, n_relay, n_comb, n_red, w;
 } eplab_tune_config;

@@ -518,7 +518,15 @@ int eplab_connect_local(eplab_ctx* const* ctxs, int n) {
 
 int eplab_set_tune_config(eplab_ctx* c, const eplab_tune_config* cfg) {
   return guarded([&] {
-    validate(cfg->w == 8 || cfg->w == 16 || cfg->w == 32, "w must be one of {8,16,32}");
+    // The reference's w (warps per worker, {8,16,32}) and n_comb (combine comm CTAs) describe
+    // Hopper roles this build does not have: every CTA is 256 threads (the GEMM engine's eight
+    // warp roles; comm workers are single warps, the warp split is eplab_set_comm_options) and the
+    // combine push is the GEMM epilogue itself. Rather than accept values that change nothing,
+    // the device config takes only w = 8 and n_comb in {0, 1}; the host eplab:: API keeps the
+    // reference's ranges for the reference model.
+    validate(cfg->w == 8, "w must be 8 on B200 (256-thread CTAs; the reference's {16,32} have no effect here)");
+    validate(cfg->n_comb == 0 || cfg->n_comb == 1,
+             "n_comb must be 0 or 1 on B200 (the combine push runs in the GEMM epilogue, no combine CTAs)");
     validate(cfg->n_disp >= 0, "n_disp must be >= 0 (0: the GEMM CTAs' spare warps move the rows)");
     validate(cfg->n_relay >= 0, "n_relay must be >= 0");
     // deadlock constraint of types.cpp:59-64; producers are claimed first, so the persistent

@@ -6,6 +6,7 @@
 #include "moe_common.cuh"
 
 #include <type_traits>
+#include <utility>
 
 namespace eplab_dev {
 
@@ -30,6 +31,19 @@ struct has_release_after<M, std::void_t<decltype(M::RELEASE_AFTER)>> : std::bool
 template <class Mode, class Args>
 __device__ __forceinline__ void call_release_after(const Args& a, const TileDesc& td, int r) {
   if constexpr (has_release_after<Mode>::value) Mode::epilogue_release(a, td, r);
+}
+
+// Debug bits of the Mode's Args (MkArgs::dbg), 0 for argument types without them. Experiments only
+// (eplab_set_option("dbg", ...)): 256 = the producer skips the B operand loads (wrong results; measures
+// what the B operand traffic costs, the bound on TMA-multicast savings).
+template <class A, class = void>
+struct has_dbg : std::false_type {};
+template <class A>
+struct has_dbg<A, std::void_t<decltype(std::declval<A>().dbg)>> : std::true_type {};
+template <class A>
+__device__ __forceinline__ int dbg_bits(const A& a) {
+  if constexpr (has_dbg<A>::value) return a.dbg;
+  return 0;
 }
 
 __device__ __forceinline__ void timeline_push(const Timeline& tl, unsigned long long t0,

@@ -124,6 +124,7 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
     // ---------------- TMA producer (both CTAs)
     if (lane == 0) {
       for (int i = 0; i < 8; ++i) tma_prefetch_desc(&tm.m[i]);
+      const bool skip_b = (dbg_bits(args) & 256) != 0;  // experiment: no B traffic (results wrong)
       const uint32_t rempty0 = mapa_shared(smem_u32(&S->rempty[0]), 0);
       uint32_t stage = 0, phase = 0;
       for (int it = 0;; ++it) {
@@ -139,11 +140,11 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
           mbar_wait_wd(&S->empty[stage], phase ^ 1, wd, 42);
           const uint32_t full0 = mapa_shared(smem_u32(&S->full[stage]), 0);
           if (leader)
-            mbar_arrive_expect_tx(&S->full[stage], 2 * P_STAGE_BYTES);
+            mbar_arrive_expect_tx(&S->full[stage], skip_b ? P_STAGE_BYTES : 2 * P_STAGE_BYTES);
           else
             mbar_arrive_cluster(full0);
           Mode::load_a_pair(args, tm, full0, sA + stage * P_HALF_BYTES, td, kb, rank);
-          Mode::load_b_pair(args, tm, full0, sB + stage * P_HALF_BYTES, td, kb, rank);
+          if (!skip_b) Mode::load_b_pair(args, tm, full0, sB + stage * P_HALF_BYTES, td, kb, rank);
           if (++stage == P_STAGES) {
             stage = 0;
             phase ^= 1;

@@ -175,8 +175,10 @@ EPLAB_API int eplab_dispatch_group_gemm(eplab_ctx* ctx, const void* d_x, const v
  * the top-k barrier and the k-ordered reduction into d_y [n_tok][H] bf16. */
 EPLAB_API int eplab_group_gemm_combine(eplab_ctx* ctx, const void* d_w_down, void* d_y,
                                        void* stream);
-/* Backward Dispatch+GroupGEMM: dY dispatch, gate gradient, down dgrad + SwiGLU backward,
- * down weight gradient (deterministic transposed GroupGEMM). */
+/* Backward Dispatch+GroupGEMM: dY dispatch, down dgrad + SwiGLU backward (whose epilogue also
+ * forms the gate-gradient partials <dY W_down, h> per column tile), down weight gradient
+ * (deterministic transposed GroupGEMM). d_dgate [n_tok][k] is completed by the following
+ * eplab_group_gemm_combine_bwd (its reduce sums the partials in tile order). */
 EPLAB_API int eplab_dispatch_group_gemm_bwd(eplab_ctx* ctx, const void* d_dy,
                                             const void* d_w_down, void* d_dw_down,
                                             float* d_dgate, void* stream);
@@ -245,8 +247,9 @@ EPLAB_API int eplab_timeline_export(eplab_ctx* ctx, const char* path, double* ov
  *   plan_counts(row[E+1]) ; AllGather rows -> rows_all[W][E+1] ; plan_finish(rows_all)
  *   pack(x, send, send_meta[n][2]) ; A2A(send, send_meta) ; scatter(recv, recv_meta, n_recv, 0)
  *   up(w_up) ; down(w_down, o_ret[n_recv]) ; A2A back -> o_src[n_send] ; combine(o_src, y, 0)
- *   pack(dy, send, NULL) ; A2A ; scatter(recv, NULL, n_recv, 1) ; dgate(dy, o_src, dgate)
- *   bwd_down(w_down, dw_down) ; bwd_up(w_up, dx_ret, dw_up) ; A2A back -> dx_src ; combine(dx_src, dx, 1)
+ *   pack(dy, send, NULL) ; A2A ; scatter(recv, NULL, n_recv, 1)
+ *   bwd_down(w_down, dw_down, dgp_ret[n_recv][F/256] f32) ; A2A back -> dgp_src ; dgate(dgp_src, dgate)
+ *   bwd_up(w_up, dx_ret, dw_up) ; A2A back -> dx_src ; combine(dx_src, dx, 1)
  * Send split to rank d = sum of rows_all[me][d*epr .. d*epr+epr); receive split from rank s = sum of
  * rows_all[s][me*epr .. me*epr+epr). Paper_2604_19241_b200/unfused.py drives it over NCCL. */
 EPLAB_API int eplab_unfused_plan_counts(eplab_ctx* ctx, const int32_t* d_topk_ids, const float* d_gate_w,
@@ -259,9 +262,9 @@ EPLAB_API int eplab_unfused_scatter(eplab_ctx* ctx, const void* d_recv, const in
 EPLAB_API int eplab_unfused_up(eplab_ctx* ctx, const void* d_w_up, void* stream);
 EPLAB_API int eplab_unfused_down(eplab_ctx* ctx, const void* d_w_down, void* d_o_ret, void* stream);
 EPLAB_API int eplab_unfused_combine(eplab_ctx* ctx, const void* d_rows, void* d_out, int phase, void* stream);
-EPLAB_API int eplab_unfused_dgate(eplab_ctx* ctx, const void* d_dy, const void* d_o_rows, float* d_dgate,
-                                  void* stream);
-EPLAB_API int eplab_unfused_bwd_down(eplab_ctx* ctx, const void* d_w_down, void* d_dw_down, void* stream);
+EPLAB_API int eplab_unfused_dgate(eplab_ctx* ctx, const float* d_dgp_src, float* d_dgate, void* stream);
+EPLAB_API int eplab_unfused_bwd_down(eplab_ctx* ctx, const void* d_w_down, void* d_dw_down, float* d_dgp_ret,
+                                     void* stream);
 EPLAB_API int eplab_unfused_bwd_up(eplab_ctx* ctx, const void* d_w_up, void* d_dx_ret, void* d_dw_up,
                                    void* stream);
 

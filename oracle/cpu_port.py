@@ -53,8 +53,9 @@ def moe_layer(sel, gw, x, w_up, w_down, dy, E, k, expand=True):
         h = _bf(g * s * u)                              # SwiGLU
         o = _bf(h @ w_down[e].t())                      # down GroupGEMM
         y_rep[idx] = o
-        dgate[idx] = (dye * o).sum(1)                   # gate gradient <dY, o>
-        dh = we[:, None] * (dye @ w_down[e])            # down dgrad
+        dyw = dye @ w_down[e]                           # down dgrad accumulator (before the gate weight)
+        dgate[idx] = (dyw * h).sum(1)                   # gate gradient <dY, o> = <dY W_down, h>
+        dh = we[:, None] * dyw
         dgu = torch.cat([_bf(dh * u * s * (1 + g * (1 - s))), _bf(dh * g * s)], 1)  # SwiGLU bwd
         hw = _bf(we[:, None] * h)
         dx_rep[idx] = _bf(dgu @ w_up[e])                # up dgrad

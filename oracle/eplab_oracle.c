@@ -614,6 +614,7 @@ int orc_moe_layer(const orc_layer_dims* d, const int32_t* sel, const float* gw,
     uint16_t* dgu = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)(R > 0 ? R : 1) * 2 * F);
     uint16_t* hw = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)(R > 0 ? R : 1) * F);
     uint16_t* dxr = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)(R > 0 ? R : 1) * H);
+    float* dgr = (float*)malloc(sizeof(float) * (size_t)(R > 0 ? R : 1));
 #pragma omp parallel for schedule(dynamic, 4)
     for (long long p = 0; p < R; ++p) {
       const long long i = rows[p];
@@ -622,9 +623,13 @@ int orc_moe_layer(const orc_layer_dims* d, const int32_t* sel, const float* gw,
       const uint16_t* dyr = dy + (size_t)(i / K) * H;
       const uint16_t* g = gu + (size_t)p * 2 * F;
       uint16_t* dg = dgu + (size_t)p * 2 * F;
+      /* gate gradient dgate = <dY, o> = <dY W_down, h>: the dgrad accumulator (before the gate
+       * weight) dotted with the bf16 h, f ascending -- the quantity the down-dgrad epilogue forms */
+      float gsum = 0.0f;
       for (int f = 0; f < F; ++f) {
         float acc = 0.0f;
         for (int nn = 0; nn < H; ++nn) acc += bf(dyr[nn]) * bf(w_down[((size_t)e * H + nn) * F + f]);
+        gsum += acc * bf(hh[(size_t)p * F + f]);
         const float dh = w * acc;
         const float gg = bf(g[f]), uu = bf(g[F + f]);
         const float s = 1.0f / (1.0f + expf(-gg));
@@ -634,6 +639,7 @@ int orc_moe_layer(const orc_layer_dims* d, const int32_t* sel, const float* gw,
         dg[F + f] = tobf(dh * si);
         hw[(size_t)p * F + f] = tobf(w * bf(hh[(size_t)p * F + f]));
       }
+      dgr[p] = gsum;
       for (int k = 0; k < H; ++k) {
         float acc = 0.0f;
         for (int c = 0; c < 2 * F; ++c) acc += bf(dg[c]) * bf(w_up[((size_t)e * 2 * F + c) * H + k]);
@@ -652,16 +658,9 @@ int orc_moe_layer(const orc_layer_dims* d, const int32_t* sel, const float* gw,
         }
       }
     }
-    if (dgate) {
-#pragma omp parallel for
-      for (long long i = 0; i < R; ++i) {
-        const uint16_t* dyr = dy + (size_t)(i / K) * H;
-        const uint16_t* orow = o + (size_t)pos[i] * H;
-        float acc = 0.0f;
-        for (int nn = 0; nn < H; ++nn) acc += bf(dyr[nn]) * bf(orow[nn]);
-        dgate[i] = acc;
-      }
-    }
+    if (dgate)
+      for (long long i = 0; i < R; ++i) dgate[i] = dgr[pos[i]];
+    free(dgr);
     if (dw_down) {
 #pragma omp parallel for collapse(2) schedule(dynamic, 8)
       for (int e = 0; e < E; ++e)

@@ -50,7 +50,7 @@ struct eplab_ctx {
   char* sym = nullptr;
   size_t sym_bytes = 0;
   size_t off_recv_x = 0, off_recv_dy = 0, off_meta = 0, off_slot_flag = 0, off_rg = 0, off_rep = 0,
-         off_rep_dx = 0, off_tok = 0, off_cnt_all = 0, off_cnt_flag = 0;
+         off_rep_dx = 0, off_tok = 0, off_cnt_all = 0, off_cnt_flag = 0, off_dgp = 0;
   SymPtrs mine{};
   Peers peers{};
   std::vector<void*> ipc_opened;
@@ -94,6 +94,8 @@ struct eplab_ctx {
   // unfused baseline scratch (eplab_unfused_*; allocated on first use): send position of every
   // routing entry [T_max*k], return position of every receive slot [M_cap], the count row for
   // the host's all-gather [E+1], and the all-gathered rows of the current plan (caller's buffer)
+  float* dgate_out = nullptr;  // the dgate of the current backward (given to the dispatch call)
+  bool dgate_set = false;
   int* uf_spos = nullptr;
   int* uf_ret_pos = nullptr;
   int* uf_counts = nullptr;
@@ -118,6 +120,7 @@ SymPtrs sym_ptrs(const eplab_ctx* c, char* base) {
   s.tok_cnt = reinterpret_cast<uint32_t*>(base + c->off_tok);
   s.cnt_all = reinterpret_cast<int*>(base + c->off_cnt_all);
   s.cnt_flag = reinterpret_cast<uint32_t*>(base + c->off_cnt_flag);
+  s.dgp = reinterpret_cast<float*>(base + c->off_dgp);
   return s;
 }
 
@@ -337,6 +340,7 @@ int eplab_init(const eplab_init_args* args, eplab_ctx** out) {
     c->off_tok = take((size_t)4 * d.T_max * 4);
     c->off_cnt_all = take((size_t)W * E * 4);
     c->off_cnt_flag = take((size_t)W * 4);
+    c->off_dgp = take(Tk * (size_t)(d.F / 256) * 4);
     c->sym_bytes = o;
     CK(cudaMalloc(&c->sym, c->sym_bytes));
     CK(cudaMemset(c->sym + c->off_meta, 0, o - c->off_meta));
@@ -678,6 +682,8 @@ int eplab_dispatch_group_gemm_bwd(eplab_ctx* c, const void* dy, const void* w_do
     a.w_down = static_cast<const __nv_bfloat16*>(w_down);
     a.dw_down = static_cast<__nv_bfloat16*>(dw_down);
     a.dgate = dgate;
+    c->dgate_out = dgate;  // completed by the backward combine's reduce (sums the partials)
+    c->dgate_set = true;
     TmaSet tm;
     tm.m[0] = c->tm_recv_dy_k;
     tm.m[1] = eplab_host::make_bf16_map(w_down, (uint64_t)c->d.epr * c->d.H, c->d.F, c->d.F, 64, 64);
@@ -701,6 +707,8 @@ int eplab_group_gemm_combine_bwd(eplab_ctx* c, const void* w_up, void* dx, void*
     MkArgs a = base_args(c);
     a.w_up = static_cast<const __nv_bfloat16*>(w_up);
     a.dx = static_cast<__nv_bfloat16*>(dx);
+    validate(c->dgate_set, "backward combine before the backward dispatch of this iteration");
+    a.dgate = c->dgate_out;
     a.dw_up = static_cast<__nv_bfloat16*>(dw_up);
     TmaSet tm;
     tm.m[0] = c->tm_dgu_k;
@@ -1142,18 +1150,17 @@ int eplab_unfused_combine(eplab_ctx* c, const void* rows, void* out, int phase, 
   });
 }
 
-int eplab_unfused_dgate(eplab_ctx* c, const void* dy, const void* o_rows, float* dgate, void* stream) {
+int eplab_unfused_dgate(eplab_ctx* c, const float* dgp_src, float* dgate, void* stream) {
   return guarded([&] {
     uf_require(c);
     CK(cudaSetDevice(c->device));
-    if (eplab_launch::unfused_dgate_launch(c->d, c->plan, static_cast<const __nv_bfloat16*>(dy),
-                                           static_cast<const __nv_bfloat16*>(o_rows), c->uf_spos, dgate, c->num_sms,
+    if (eplab_launch::unfused_dgate_launch(c->d, c->plan, dgp_src, c->uf_spos, dgate, c->num_sms,
                                            (cudaStream_t)stream))
       throw Fail{EPLAB_ERR_INTERNAL, std::string("unfused dgate: ") + cudaGetErrorString(cudaGetLastError())};
   });
 }
 
-int eplab_unfused_bwd_down(eplab_ctx* c, const void* w_down, void* dw_down, void* stream) {
+int eplab_unfused_bwd_down(eplab_ctx* c, const void* w_down, void* dw_down, float* dgp_ret, void* stream) {
   return guarded([&] {
     uf_require(c);
     CK(cudaSetDevice(c->device));
@@ -1162,6 +1169,7 @@ int eplab_unfused_bwd_down(eplab_ctx* c, const void* w_down, void* dw_down, void
     MkArgs a = uf_args(c);
     a.w_down = static_cast<const __nv_bfloat16*>(w_down);
     a.dw_down = static_cast<__nv_bfloat16*>(dw_down);
+    a.ret_dgp = dgp_ret;
     TmaSet tm;
     tm.m[0] = c->tm_recv_dy_k;
     tm.m[1] = eplab_host::make_bf16_map(w_down, (uint64_t)c->d.epr * c->d.H, c->d.F, c->d.F, 64, 64);

@@ -21,8 +21,8 @@ int unfused_scatter_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p
                            eplab_dev::SlotMeta* meta, int* ret_pos, int sms, cudaStream_t st);
 int unfused_fold_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p, const __nv_bfloat16* rows,
                         const int* spos, __nv_bfloat16* out, int ph, int sms, cudaStream_t st);
-int unfused_dgate_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p, const __nv_bfloat16* dy,
-                         const __nv_bfloat16* rows, const int* spos, float* dgate, int sms, cudaStream_t st);
+int unfused_dgate_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p, const float* parts,
+                         const int* spos, float* dgate, int sms, cudaStream_t st);
 int zero_padding_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p,
                         __nv_bfloat16* recv, cudaStream_t st);
 int launch_fwd_dispatch(const eplab_dev::TmaSet& tm, const eplab_dev::MkArgs& a, int grid,

@@ -62,6 +62,11 @@ struct GemmSmem {
   int pend[2];      // CTA pair: first non-pre task id of each CTA (leader's copy)
   int post_ids[4];  // CTA pair: claimed non-tile ids to hand out after the GEMM phase
   int post_n;
+  // CTA pair, Modes with a release warp: the epilogue warps queue each finished tile here and warp
+  // 2 publishes it (fence + scoreboard updates) off the epilogue's critical path
+  uint64_t rq_full[4];   // 4 arrivals: the four epilogue warps queued the tile
+  uint64_t rq_empty[4];  // 1 arrival: the release warp published it
+  TileDesc rq_td[4];
   // comm role (runs before the CTA enters the GEMM roles; reuses the stage buffers)
   uint64_t cbar[48];      // one mbarrier per bulk-copy slot
   uint32_t cphase[4];     // per issuer: parity bit per owned slot (carried across comm tasks)

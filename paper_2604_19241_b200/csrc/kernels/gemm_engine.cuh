@@ -33,6 +33,18 @@ __device__ __forceinline__ void call_release_after(const Args& a, const TileDesc
   if constexpr (has_release_after<Mode>::value) Mode::epilogue_release(a, td, r);
 }
 
+// A Mode with `static constexpr bool RELEASE_WARP = true` (CTA-pair engine) has its tiles published
+// by warp 2 instead of the epilogue warps: `Mode::wants_release(args, tile)` selects the tiles and
+// `Mode::release_tile(args, tile, lane)` publishes one (a warp-wide job).
+template <class M, class = void>
+struct has_release_warp : std::false_type {};
+template <class M>
+struct has_release_warp<M, std::void_t<decltype(M::RELEASE_WARP)>> : std::bool_constant<M::RELEASE_WARP> {};
+template <class Mode, class Args>
+__device__ __forceinline__ void call_release_tile(const Args& a, const TileDesc& td, int lane) {
+  if constexpr (has_release_warp<Mode>::value) Mode::release_tile(a, td, lane);
+}
+
 // Debug bits of the Mode's Args (MkArgs::dbg), 0 for argument types without them. Experiments only
 // (eplab_set_option("dbg", ...)): 256 = the producer skips the B operand loads (wrong results; measures
 // what the B operand traffic costs, the bound on TMA-multicast savings).

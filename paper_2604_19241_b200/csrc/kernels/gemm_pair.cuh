@@ -39,7 +39,11 @@ __device__ __forceinline__ void gemm_setup_pair(GemmSmem* S, uint32_t rank) {
       mbar_init(&S->rempty[i], 11);  // leader: producer, mma, 4 epi; peer: producer, 4 epi
     }
     for (int i = 0; i < 48; ++i) mbar_init(&S->cbar[i], 1);
-    for (int i = 0; i < 4; ++i) S->cphase[i] = 0;
+    for (int i = 0; i < 4; ++i) {
+      S->cphase[i] = 0;
+      mbar_init(&S->rq_full[i], 4);
+      mbar_init(&S->rq_empty[i], 1);
+    }
     S->bcast = TASK_STOP;
     fence_mbar_init();
   }
@@ -73,7 +77,21 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
   // spare warps: warp 2 (TMEM owner, idle between allocation and teardown) of both CTAs and the
   // non-leader's warps 1 and 3 (the leader alone issues MMAs and schedules)
   const bool spare = warp == 2 || (!leader && (warp == 1 || warp == 3));
-  if (has_spare<Mode>::value && spare) {
+  constexpr bool kRelWarp = has_release_warp<Mode>::value;
+  if (kRelWarp && warp == 2) {
+    // ---------------- release warp (both CTAs): publishes the tiles the epilogue warps queue --
+    // the system/gpu-scope fence waits for the tile's stores to complete, which would otherwise
+    // stall the epilogue warps for the next accumulator (Qwen3 fwd combine: 30 % of the span)
+    for (int it = 0;; ++it) {
+      const int slot = it & 3;
+      mbar_wait(&S->rq_full[slot], (it >> 2) & 1);  // acquire (CTA): the four warps' stores
+      const TileDesc td = S->rq_td[slot];
+      if (td.rows < 0) break;
+      call_release_tile<Mode>(args, td, (int)lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S->rq_empty[slot]);
+    }
+  } else if (has_spare<Mode>::value && spare) {
     call_spare<Mode>(args, tl);
   } else if (warp == 3) {
     if (leader && lane == 0) {
@@ -213,6 +231,19 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
     const int r = q * 32 + (int)lane;
     const uint32_t rempty0 = mapa_shared(smem_u32(&S->rempty[0]), 0);
     const uint32_t tempty0 = mapa_shared(smem_u32(&S->tempty[0]), 0);
+    // stall accounting of epilogue warp 0 (timeline on): waiting for the accumulator (MMA), the
+    // epilogue itself (TMEM -> registers -> stores), the release after the accumulator hand-back
+    const bool acct = tl.rec != nullptr && q == 0;
+    unsigned long long e_wait = 0, e_epi = 0, e_rel = 0, e_begin = acct ? globaltimer() : 0, tw = 0;
+    int rq_it = 0;  // tiles queued for the release warp (the same sequence in all four warps)
+    auto queue_release = [&](const TileDesc& h) {
+      const int s = rq_it & 3;
+      mbar_wait(&S->rq_empty[s], ((rq_it >> 2) & 1) ^ 1);
+      if (q == 0 && lane == 0) S->rq_td[s] = h;
+      __syncwarp();  // every lane's pushed rows precede the arrival (release, CTA scope)
+      if (lane == 0) mbar_arrive(&S->rq_full[s]);
+      ++rq_it;
+    };
     for (int it = 0;; ++it) {
       const int slot = it % RING;
       mbar_wait_cluster_wd(&S->rfull[slot], (it / RING) & 1, wd, 46);
@@ -222,20 +253,44 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
       if (lane == 0) mbar_arrive_cluster(rempty0 + slot * 8);
       if (t == TASK_STOP) {
         if (lane == 0) tma_store_wait<0>();
+        if constexpr (kRelWarp) {
+          TileDesc stop{};
+          stop.rows = -1;
+          queue_release(stop);
+        }
         break;
       }
       const TileDesc half = Mode::half_of(td, rank);
       const bool work = Mode::half_has_work(half);
       if (work) Mode::epilogue_prefetch(args, half, r);
       const uint32_t acc = it & 1;
+      if (acct) tw = globaltimer();
       mbar_wait_wd(&S->tfull[acc], (it >> 1) & 1, wd, 47);
       tc_fence_after();
+      if (acct) {
+        const unsigned long long now = globaltimer();
+        e_wait += now - tw;
+        tw = now;
+      }
       const uint32_t taddr = S->tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
       if (work) Mode::epilogue(args, tm, half, taddr, r, tiles_smem + TILES_BYTES + q * EPI_WARP_BYTES);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
-      if (work) call_release_after<Mode>(args, half, r);
+      if (acct) {
+        const unsigned long long now = globaltimer();
+        e_epi += now - tw;
+        tw = now;
+      }
+      if constexpr (kRelWarp) {
+        if (work && Mode::wants_release(args, half)) queue_release(half);
+      } else {
+        if (work) call_release_after<Mode>(args, half, r);
+      }
+      if (acct) {
+        __syncwarp();
+        e_rel += globaltimer() - tw;
+      }
       if (Mode::HAS_TILE_DONE || tl.rec) {
         epi_bar();
         if (warp == 4 && lane == 0) {
@@ -243,6 +298,11 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
           if (leader) timeline_push(tl, S->tstart[it & 7], globaltimer(), ROLE_COMP, t + tile_lo);
         }
       }
+    }
+    if (acct && lane == 0) {  // three records per CTA, durations = the totals (task -9004..-9006)
+      timeline_push(tl, e_begin, e_begin + e_wait, ROLE_COMP, -9004);
+      timeline_push(tl, e_begin, e_begin + e_epi, ROLE_COMP, -9005);
+      timeline_push(tl, e_begin, e_begin + e_rel, ROLE_COMP, -9006);
     }
   }
   __syncthreads();

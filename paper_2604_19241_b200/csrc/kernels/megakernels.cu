@@ -355,10 +355,9 @@ __device__ void comm_pipeline(const MkArgs& a, int ph, GemmSmem* S, uint8_t* sbu
 // (token_map.cpp:108-126), claimed in order from one atomic round counter by every comm
 // worker -- the 8 warps of each comm CTA (SM split, n_disp) and the spare warps of the GEMM
 // CTAs (warp split: warp 2 of both CTAs of a pair, warps 1 and 3 of the non-leader CTA). A
-// warp moves its round with 16-byte loads/stores, two rows in flight (16 x 16 B per lane); in
-// the backward phase it folds the gate gradient <dY_t, o_{t,j}> of every item while the dY row
-// is in registers. Then it releases the round: one system-scope fence, relaxed rowgroup
-// counter updates aggregated per counter (relay off) or per-slot epoch flags (relay on).
+// warp moves its round with 16-byte loads/stores, two rows in flight (16 x 16 B per lane). Then
+// it releases the round: one system-scope fence, relaxed rowgroup counter updates aggregated per
+// counter (relay off) or per-slot epoch flags (relay on).
 constexpr int CROUNDS = 128;
 __device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
   const Dims& d = a.d;
@@ -427,7 +426,11 @@ __device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
   auto progress = [&]() {
     if (n_copies <= 2) release();
   };
-  if (ph == 0) {
+  // x rows (forward) and dY rows (backward) alike: a pure row copy, two rows in flight. (The gate
+  // gradient is no longer folded here: the down-dgrad epilogue has <dY W_down, h> per row in
+  // registers, so the comm warps no longer read the o replica rows -- a third of the backward
+  // dispatch's bytes.)
+  {
     unsigned m = __ballot_sync(0xffffffffu, dst >= 0);
     while (m) {
       const int qa = __ffs(m) - 1;
@@ -460,42 +463,6 @@ __device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
       copied |= (1u << qa) | (1u << qb);
       n_copies += two ? 2 : 1;
       progress();
-    }
-  } else {
-    const int4* orow_base = reinterpret_cast<const int4*>(a.peers.p[me].rep);
-    unsigned m = __ballot_sync(0xffffffffu, item >= 0);
-    while (m) {
-      const int q = __ffs(m) - 1;
-      m &= m - 1;
-      const int i = __shfl_sync(0xffffffffu, item, q);
-      const int dq = __shfl_sync(0xffffffffu, dst, q), sq = __shfl_sync(0xffffffffu, slot, q);
-      const int4* src = src_base + (size_t)(i / k) * vecs;
-      const int4* orow = orow_base + (size_t)i * vecs;
-      int4* drow = dq >= 0 ? dst_row(dq, sq) : nullptr;
-      float gacc = 0.f;
-      for (int c = lane; c < vecs; c += 256) {
-        int4 v[8], o[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (c + 32 * u < vecs) {
-            v[u] = ld_nc_v4(src + c + 32 * u);
-            o[u] = ld_nc_v4(orow + c + 32 * u);
-          }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (c + 32 * u < vecs) {
-            if (drow) drow[c + 32 * u] = v[u];
-            gacc = dot8_bf16(v[u], o[u], gacc);
-          }
-      }
-#pragma unroll
-      for (int s2 = 16; s2 > 0; s2 >>= 1) gacc += __shfl_xor_sync(0xffffffffu, gacc, s2);
-      if (lane == 0) a.dgate[i] = gacc;
-      if (dq >= 0) {
-        copied |= 1u << q;
-        ++n_copies;
-        progress();
-      }
     }
   }
   release();
@@ -575,29 +542,6 @@ __device__ void comm_task(const MkArgs& a, int task, int ph, GemmSmem* S, uint8_
           comm_pipeline<12, 2>(a, ph, S, sbuf, cnt, warp);
       }
       __syncwarp();
-    } else if (ph == 1) {
-      const int vecs = H / 8;
-      for (int q = warp - n_iss; q < cnt; q += GEMM_THREADS / 32 - n_iss) {
-        const int i = S->citem[q], t = i / k;
-        const int4* src = reinterpret_cast<const int4*>(a.dy + (size_t)t * H);
-        const int4* orow = reinterpret_cast<const int4*>(a.peers.p[me].rep + (size_t)i * H);
-        float gacc = 0.f;
-        int c = lane;
-        for (; c + 7 * 32 < vecs; c += 8 * 32) {
-          int4 v[8], o[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            v[u] = ld_nc_v4(src + c + u * 32);
-            o[u] = ld_nc_v4(orow + c + u * 32);
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) gacc = dot8_bf16(v[u], o[u], gacc);
-        }
-        for (; c < vecs; c += 32) gacc = dot8_bf16(ld_nc_v4(src + c), ld_nc_v4(orow + c), gacc);
-#pragma unroll
-        for (int s = 16; s > 0; s >>= 1) gacc += __shfl_xor_sync(0xffffffffu, gacc, s);
-        if (lane == 0) a.dgate[i] = gacc;
-      }
     }
     __syncthreads();
   }
@@ -763,6 +707,13 @@ __device__ __forceinline__ void fold_token(const MkArgs& a, int ph, long long t)
       o.w = (int)pack_bf16(acc[u][6], acc[u][7]);
       out[(size_t)t * vecs + c + 32 * u] = o;
     }
+  }
+  if (ph == 1 && lane < k) {  // the token's gate gradients: its k entries' partials, tiles in order
+    const int ncb = d.F / BN;
+    const float* g = me.dgp + ((size_t)t * k + lane) * ncb;
+    float s = g[0];
+    for (int c = 1; c < ncb; ++c) s = __fadd_rn(s, g[c]);
+    a.dgate[t * k + lane] = s;
   }
 }
 
@@ -994,6 +945,23 @@ __device__ __forceinline__ void push_release(const MkArgs& a, const TileDesc& td
   red_relaxed_sys_add(tok_counter(a.peers.p[mt.src], a.d, ph, PAR(a), mt.rep / a.d.topk), 1u);
 }
 
+// The same publication for a whole (half) tile, by the CTA's release warp (CTA-pair engine): the
+// four epilogue warps' row stores happen-before this warp through the release queue's mbarrier
+// (release / acquire at CTA scope), so ONE cumulative fence of this warp orders all 128 rows before
+// the counter updates; the epilogue warps go straight on to the next accumulator.
+__device__ __forceinline__ void push_release_tile(const MkArgs& a, const TileDesc& td, int lane, int ph) {
+  if (a.unfused) return;
+  if (a.d.world == 1)
+    fence_acq_rel_gpu();  // one GPU: the reducer is on this device
+  else
+    fence_acq_rel_sys();
+  const SymPtrs& me = a.peers.p[a.d.rank];
+  for (int r = lane; r < td.rows; r += 32) {
+    const SlotMeta mt = me.meta[td.m0 + r];
+    red_relaxed_sys_add(tok_counter(a.peers.p[mt.src], a.d, ph, PAR(a), mt.rep / a.d.topk), 1u);
+  }
+}
+
 // Pull this row's slot metadata (return address / gate weight) into L1 before the accumulator
 // is ready, so the epilogue's first dependent load does not wait on L2.
 __device__ __forceinline__ void prefetch_meta_l1(const MkArgs& a, const TileDesc& td, int r) {
@@ -1005,8 +973,11 @@ __device__ __forceinline__ void prefetch_meta_l1(const MkArgs& a, const TileDesc
 struct ModeDown {
   using Args = MkArgs;
   static constexpr bool HAS_TILE_DONE = false;
-  static constexpr bool RELEASE_AFTER = true;
+  static constexpr bool RELEASE_AFTER = true;   // single-CTA engine: per-row release by the epilogue
+  static constexpr bool RELEASE_WARP = true;    // CTA-pair engine: per-tile release by warp 2
   __device__ static void epilogue_release(const Args& a, const TileDesc& td, int r) { push_release(a, td, r, 0); }
+  __device__ static bool wants_release(const Args& a, const TileDesc&) { return !a.unfused; }
+  __device__ static void release_tile(const Args& a, const TileDesc& td, int lane) { push_release_tile(a, td, lane, 0); }
   __device__ static void epilogue_prefetch(const Args& a, const TileDesc& td, int r) { prefetch_meta_l1(a, td, r); }
   __device__ static TileDesc tile_pair(const Args& a, int t) {
     return nt_tile_pair(a.d, a.p, t, a.d.H / BN, BN, a.d.F / BK, a.rgp);
@@ -1178,7 +1149,13 @@ struct ModeDgradDown {
     const size_t m = (size_t)td.m0 + r;
     const int row0 = td.m0 + (r & ~31);
     const bool live = r < td.rows;
-    const float w = live ? a.peers.p[a.d.rank].meta[m].w : 0.f;
+    SlotMeta mt{0, 0, 0.f, 0};
+    if (live) mt = a.peers.p[a.d.rank].meta[m];
+    const float w = mt.w;
+    // gate gradient: dgate_{t,j} = <dY_t, o_{t,j}> = <dY_t W_down, h_{t,j}> -- the accumulator
+    // before the gate weight, dotted with the (recomputed bf16) h, fp32 fmaf in column order; one
+    // partial per (row, column tile), summed over the tiles in order by the source's reduce
+    float gpart = 0.f;
     const int4* gsrc = reinterpret_cast<const int4*>(a.gu + m * 2 * F + td.n0);
     const int4* usrc = reinterpret_cast<const int4*>(a.gu + m * 2 * F + F + td.n0);
     // saved g, u of chunk c+1 are in flight while chunk c is computed (software pipelining)
@@ -1221,6 +1198,7 @@ struct ModeDgradDown {
             dg[h] = dh * uu[h] * ds;
             du[h] = dh * si;
             hv[h] = w * hh;
+            gpart = fmaf(v[2 * q + h], hh, gpart);
           }
           pdg[q] = pack_bf16(dg[0], dg[1]);
           pdu[q] = pack_bf16(du[0], du[1]);
@@ -1254,6 +1232,12 @@ struct ModeDgradDown {
         }
       }
     }
+    if (live) {  // this tile's gate-gradient partial, to the source (peer memory at EP > 1)
+      const int ncb = F / BN;
+      float* dst = a.unfused ? a.ret_dgp + (size_t)a.ret_pos[m] * ncb
+                             : a.peers.p[mt.src].dgp + (size_t)mt.rep * ncb;
+      dst[td.pad0] = gpart;
+    }
     // the weight-gradient tiles of this (expert, f-block) read HW / dGU through TMA: complete
     // the stores before tile_done publishes the count
     if (lane == 0) {
@@ -1279,6 +1263,10 @@ struct ModeDgradUp {
   __device__ static void epilogue_release(const Args& a, const TileDesc& td, int r) {
     if (!td.pad1) push_release(a, td, r, 1);  // dgrad tiles push dX replicas; wgrad tiles do not
   }
+  static constexpr bool RELEASE_WARP = true;  // CTA pair: warp 2 publishes; the non-leader's warps
+                                              // 1 and 3 remain the spare reduce workers
+  __device__ static bool wants_release(const Args& a, const TileDesc& td) { return !a.unfused && !td.pad1; }
+  __device__ static void release_tile(const Args& a, const TileDesc& td, int lane) { push_release_tile(a, td, lane, 1); }
   static constexpr bool SPARE = true;
   __device__ static void spare(const Args& a, const Timeline& tl) { spare_reduce(a, tl, 1); }
   __device__ static void epilogue_prefetch(const Args& a, const TileDesc& td, int r) { prefetch_meta_l1(a, td, r); }

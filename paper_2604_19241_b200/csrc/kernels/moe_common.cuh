@@ -12,6 +12,8 @@
 //     tok_cnt  [2 ph][2 par][T_max] u32 replica column-tiles landed per source token
 //     cnt_all  [W][E]       i32   AllGather of per-expert counts (Alg. 1 line 3)
 //     cnt_flag [W]          u32   epoch flags of cnt_all rows
+//     dgp      [T_max*k][F/256] f32  gate-gradient partials <dY W_down, h> per down-dgrad column
+//                                    tile, written by the expert rank, summed by the source's reduce
 //   local region: GU [M_cap][2F], Hact [M_cap][F], dGU [M_cap][2F], HW [M_cap][F] bf16,
 //     plan arrays (per source entry: dst slot / offset / local index; schedule), per-expert
 //     receive geometry and tile prefixes.
@@ -48,6 +50,7 @@ struct SymPtrs {
   uint32_t* tok_cnt;
   int* cnt_all;
   uint32_t* cnt_flag;
+  float* dgp;  // [T_max*k][F/256] gate-gradient partials at the source, one per down-dgrad column tile
 };
 
 struct Peers {
@@ -151,6 +154,7 @@ struct MkArgs {
   int unfused;
   __nv_bfloat16* ret;
   const int* ret_pos;
+  float* ret_dgp;  // unfused: gate-gradient partials [n_recv][F/256] in the return all-to-all's order
 };
 
 #ifdef __CUDACC__

@@ -13,7 +13,7 @@
 //              of the fused path (128-aligned expert segments in global (src, t, j) order, Alg. 1
 //              final_idx) + slot metadata + the slot's position in the return all-to-all
 //   fold     : the k-ascending reference fold over the returned rows (precision.cpp:31-37)
-//   dgate    : <dY_t, o_{t,j}> at the source, in the fused comm warps' lane order
+//   dgate    : the sum of the returned gate-gradient partials, in the fused reduce's order
 #include <algorithm>
 
 #include "moe_common.cuh"
@@ -133,22 +133,19 @@ __global__ void __launch_bounds__(256) unfused_fold_kernel(Dims d, PlanDev p, co
   }
 }
 
-// One warp per routing entry: dgate_{t,j} = <dY_t, o_{t,j}>, each lane over its 16-byte chunks
-// lane, lane + 32, ... in increasing order, then the xor tree -- the fused comm warps' order.
-__global__ void __launch_bounds__(256) unfused_dgate_kernel(Dims d, PlanDev p, const __nv_bfloat16* dy,
-                                                            const __nv_bfloat16* rows, const int* spos,
-                                                            float* dgate) {
+// One thread per routing entry: dgate_{t,j} = the sum of the entry's gate-gradient partials
+// <dY W_down, h> over the down-dgrad column tiles (returned by the all-to-all), in tile order -- the
+// fused reduce role's sum.
+__global__ void __launch_bounds__(256) unfused_dgate_kernel(Dims d, PlanDev p, const float* parts,
+                                                            const int* spos, float* dgate) {
   if (p.scalars[3]) return;
-  const int lane = threadIdx.x & 31, vecs = d.H / 8, k = d.topk;
-  const long long n = (long long)p.n_tok * k;
-  for (long long i = (long long)blockIdx.x * 8 + (threadIdx.x >> 5); i < n; i += (long long)gridDim.x * 8) {
-    const int4* a = reinterpret_cast<const int4*>(dy + (size_t)(i / k) * d.H);
-    const int4* b = reinterpret_cast<const int4*>(rows + (size_t)spos[i] * d.H);
-    float g = 0.f;
-    for (int c = lane; c < vecs; c += 32) g = dot8_bf16(ld_nc_v4(a + c), ld_nc_v4(b + c), g);
-#pragma unroll
-    for (int s = 16; s > 0; s >>= 1) g += __shfl_xor_sync(0xffffffffu, g, s);
-    if (lane == 0) dgate[i] = g;
+  const int ncb = d.F / 256;
+  const long long n = (long long)p.n_tok * d.topk;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const float* g = parts + (size_t)spos[i] * ncb;
+    float s = g[0];
+    for (int c = 1; c < ncb; ++c) s = __fadd_rn(s, g[c]);
+    dgate[i] = s;
   }
 }
 
@@ -179,9 +176,11 @@ int unfused_fold_launch(const Dims& d, const PlanDev& p, const __nv_bfloat16* ro
   unfused_fold_kernel<<<grid_for(p.n_tok, sms), 256, 0, st>>>(d, p, rows, spos, out, ph);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
-int unfused_dgate_launch(const Dims& d, const PlanDev& p, const __nv_bfloat16* dy, const __nv_bfloat16* rows,
-                         const int* spos, float* dgate, int sms, cudaStream_t st) {
-  unfused_dgate_kernel<<<grid_for((long long)p.n_tok * d.topk, sms), 256, 0, st>>>(d, p, dy, rows, spos, dgate);
+int unfused_dgate_launch(const Dims& d, const PlanDev& p, const float* parts, const int* spos, float* dgate,
+                         int sms, cudaStream_t st) {
+  const long long n = (long long)p.n_tok * d.topk;
+  const int grid = (int)std::max(1LL, std::min((n + 255) / 256, (long long)sms * 8));
+  unfused_dgate_kernel<<<grid, 256, 0, st>>>(d, p, parts, spos, dgate);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 

@@ -29,8 +29,8 @@ _SIGS = {
     "eplab_unfused_up": [_P, _P, _P],
     "eplab_unfused_down": [_P, _P, _P, _P],
     "eplab_unfused_combine": [_P, _P, _P, _I, _P],
-    "eplab_unfused_dgate": [_P, _P, _P, _P, _P],
-    "eplab_unfused_bwd_down": [_P, _P, _P, _P],
+    "eplab_unfused_dgate": [_P, _P, _P, _P],
+    "eplab_unfused_bwd_down": [_P, _P, _P, _P, _P],
     "eplab_unfused_bwd_up": [_P, _P, _P, _P, _P],
 }
 
@@ -83,11 +83,11 @@ class UnfusedEpMoE(EpMoE):
     def combine(self, rows, out, phase, stream=None):
         _check(_lib().eplab_unfused_combine(self.h, _ptr(rows), _ptr(out), phase, _stream(stream)))
 
-    def dgate(self, dy, o_rows, dgate, stream=None):
-        _check(_lib().eplab_unfused_dgate(self.h, _ptr(dy), _ptr(o_rows), _ptr(dgate), _stream(stream)))
+    def dgate(self, dgp_src, dgate, stream=None):
+        _check(_lib().eplab_unfused_dgate(self.h, _ptr(dgp_src), _ptr(dgate), _stream(stream)))
 
-    def bwd_down(self, w_down, dw_down, stream=None):
-        _check(_lib().eplab_unfused_bwd_down(self.h, _ptr(w_down), _ptr(dw_down), _stream(stream)))
+    def bwd_down(self, w_down, dw_down, dgp_ret, stream=None):
+        _check(_lib().eplab_unfused_bwd_down(self.h, _ptr(w_down), _ptr(dw_down), _ptr(dgp_ret), _stream(stream)))
 
     def bwd_up(self, w_up, dx_ret, dw_up, stream=None):
         _check(_lib().eplab_unfused_bwd_up(self.h, _ptr(w_up), _ptr(dx_ret), _ptr(dw_up), _stream(stream)))
@@ -184,17 +184,20 @@ def unfused_step(layers, comm, xs, ids, gws, dys, w_ups, w_downs, stream=None):
     for r, L in enumerate(layers):
         L.pack(dys[r], send[r], None, stream)
     recv = comm.all_to_all(send, ss, rs, H, bf16)
-    grads, dx_ret = [], []
+    ncb = layers[0].F // 256  # gate-gradient partials per row: one per down-dgrad column tile
+    grads, dx_ret, dgp_ret = [], [], []
     for r, L in enumerate(layers):
         L.scatter(recv[r], None, n_recv[r], 1, stream)
         g = dict(dx=torch.empty_like(xs[r]), dgate=torch.empty(ids[r].shape, dtype=torch.float32, device=dev),
                  dw_up=torch.empty_like(w_ups[r]), dw_down=torch.empty_like(w_downs[r]))
-        L.dgate(dys[r], o_src[r], g["dgate"], stream)
-        L.bwd_down(w_downs[r], g["dw_down"], stream)
+        dgp_ret.append(torch.empty(n_recv[r], ncb, dtype=torch.float32, device=dev))
+        L.bwd_down(w_downs[r], g["dw_down"], dgp_ret[r], stream)
         dx_ret.append(torch.empty(n_recv[r], H, dtype=bf16, device=dev))
         L.bwd_up(w_ups[r], dx_ret[r], g["dw_up"], stream)
         grads.append(g)
+    dgp_src = comm.all_to_all(dgp_ret, rs, ss, ncb, torch.float32)
     dx_src = comm.all_to_all(dx_ret, rs, ss, H, bf16)
     for r, L in enumerate(layers):
+        L.dgate(dgp_src[r], grads[r]["dgate"], stream)
         L.combine(dx_src[r], grads[r]["dx"], 1, stream)
     return ys, grads

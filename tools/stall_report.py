@@ -1,0 +1,69 @@
+"""Stall accounting of the GEMM roles per MegaKernel (device timeline on, one EP=1 step):
+MMA issuer (per CTA pair): waiting for a tile (scheduler / scoreboard), for a free accumulator
+(epilogue), for operand stages (TMA producer); epilogue warp 0 (per CTA): waiting for the
+accumulator, the epilogue, the release after the hand-back -- each as % of the kernel's tile span.
+  python tools/step_profile.py-like: python tools/stall_report.py --config qwen3 [--opt dbg=0 ...]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2604_19241_b200 import moe as M  # noqa: E402
+from paper_2604_19241_b200.model import choose_config  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="qwen3")
+ap.add_argument("--opt", action="append", default=[], help="eplab_set_option name=value")
+ap.add_argument("--out", default="gpurun_out")
+args = ap.parse_args()
+H, F, E, k, T = bench.CONFIGS[args.config]
+inp = bench.make_inputs(args.config, 1, 0)
+L = M.EpMoE(H, F, E, k, T)
+L.set_tune_config(choose_config(H, F, E, k, T, 1))
+for o in args.opt:
+    n, v = o.split("=")
+    L.set_option(n, int(v))
+y = torch.empty(T, H, device="cuda", dtype=torch.bfloat16)
+out = dict(dx=torch.empty(T, H, dtype=torch.bfloat16, device="cuda"), dw_up=torch.empty_like(inp["w_up"]),
+           dw_down=torch.empty_like(inp["w_down"]), dgate=torch.empty(T, k, dtype=torch.float32, device="cuda"))
+steps = [("fwd_dispatch", lambda: (L.plan(inp["ids"], inp["gws"]), L.dispatch_group_gemm(inp["x"], inp["w_up"]))),
+         ("fwd_combine", lambda: L.group_gemm_combine(inp["w_down"], y)),
+         ("bwd_dispatch", lambda: L._dispatch_bwd(inp["dy"], inp["w_down"], out)),
+         ("bwd_combine", lambda: L._combine_bwd(inp["w_up"], out))]
+for _, fn in steps:  # warm-up step
+    fn()
+L.check()
+L.timeline_enable(1 << 20)
+os.makedirs(args.out, exist_ok=True)
+NAMES = {-9001: "mma_wait_tile", -9002: "mma_wait_acc", -9003: "mma_wait_ops",
+         -9004: "epi_wait_acc", -9005: "epi_work", -9006: "epi_release"}
+rep = {"config": args.config, "opts": args.opt}
+for name, fn in steps:
+    torch.cuda.synchronize()
+    fn()
+    torch.cuda.synchronize()
+    path = os.path.join(args.out, f"stall_{args.config}_{name}.json")
+    L.timeline_export(path)
+    ev = json.load(open(path))["traceEvents"]
+    tiles = [e for e in ev if e["name"] == "comp" and e["args"]["task"] >= 0]
+    if not tiles:
+        continue
+    t0 = min(e["ts"] for e in tiles)
+    t1 = max(e["ts"] + e["dur"] for e in tiles)
+    span = t1 - t0
+    acc = {}
+    for e in ev:
+        tid = e["args"]["task"]
+        if tid in NAMES:
+            a = acc.setdefault(NAMES[tid], [0.0, 0])
+            a[0] += e["dur"]
+            a[1] += 1
+    rep[name] = {"tile_span_us": round(span, 1), "tiles": len(tiles),
+                 **{n: round(100.0 * s / c / span, 1) for n, (s, c) in acc.items()}}
+L.check()
+print(json.dumps(rep), flush=True)

@@ -122,7 +122,7 @@ def hbm_bytes_per_step(cfg_name, world):
     w_up, w_down = El * 2 * F * H * 2, El * H * F * 2
     fwd_d = T * row + R * row + R * row + w_up + R * 2 * F * 2 + R * F * 2
     fwd_c = R * F * 2 + w_down + R * row + T * k * row + T * row
-    bwd_d = T * row + R * row + T * k * row + R * row + w_down + R * 2 * F * 2 + R * 2 * F * 2 + R * F * 2 \
+    bwd_d = T * row + R * row + R * row + w_down + R * 2 * F * 2 + R * 2 * F * 2 + R * F * 2 \
         + R * row + R * F * 2 + w_down
     bwd_c = R * 4 * F + w_up + R * row + R * 4 * F + R * row + w_up + T * k * row + T * row
     return float(fwd_d + fwd_c + bwd_d + bwd_c)

@@ -499,8 +499,8 @@ LayerPrediction predict_layer(const MoEShape& m, const HardwareSpec& s, const Tu
   const double w_up = epr * 2 * F * H * 2, w_down = epr * H * F * 2;
   const double b_fd = T * S + rows * S + rows * S + w_up + rows * 2 * F * 2 + rows * F * 2;
   const double b_fc = rows * F * 2 + w_down + rows * S + T * m.topk * S + T * S;
-  const double b_bd = T * S + rows * S + T * m.topk * S + rows * S + w_down + rows * 4 * F * 2 +
-                      rows * F * 2 + rows * S + rows * F * 2 + w_down;
+  const double b_bd = T * S + rows * S + rows * S + w_down + rows * 4 * F * 2 + rows * F * 2 + rows * S +
+                      rows * F * 2 + w_down;
   const double b_bc = rows * 4 * F + w_up + rows * S + rows * 4 * F + rows * S + w_up + T * m.topk * S + T * S;
   // persistent grid: SM-seconds spread over n_sm, but never less than whole waves of the
   // kernel's dominant tile (quantisation matters for small batches); the HBM traffic overlaps
@@ -519,11 +519,15 @@ LayerPrediction predict_layer(const MoEShape& m, const HardwareSpec& s, const Tu
                           mblocks * (F / 128), tile_t(H, kEpiUp), b_fd);
   const double down = mblocks * (H / 256) * tile_t(F, kEpiPush);
   p.fwd_combine = kernel(down, l_push, l_reduce, mblocks * (H / 256), tile_t(F, kEpiPush), b_fc);
-  // backward (dY dispatch also folds the gate gradient: + k*S of replica reads per token)
-  const double l_comm_b = l_comm + T * m.topk * S / (comm_units * k.comm_bw_per_sm);
+  // backward: the dY dispatch moves the forward's rows (the gate gradient is formed in the
+  // down-dgrad epilogue) with twice the comm CTAs (eplab_dispatch_group_gemm_bwd)
+  const double comm_units_b = std::max(std::min(2.0 * c.n_disp, s.n_sm / 2.0 - c.n_relay) + k.spare_sm_equiv, 1e-3);
+  const double l_comm_b = std::max(sent_rows * S / (comm_units_b * k.comm_bw_per_sm),
+                                   W > 1 ? nvl_rows * S / s.bw_nvl : 0.0);
   const double ddown = mblocks * (F / 256) * tile_t(H, kEpiDgrad);
   const double wg_down = epr * (H / 128) * (F / 256) * tile_t(seg_pad, kEpiWgrad);
-  p.bwd_dispatch = kernel(ddown + wg_down + c.n_disp * l_comm_b + c.n_relay * l_relay,
+  p.bwd_dispatch = kernel(ddown + wg_down + std::min(2.0 * c.n_disp, s.n_sm / 2.0 - c.n_relay) * l_comm_b +
+                              c.n_relay * l_relay,
                           std::max(l_comm_b, l_relay) + tile_t(H, kEpiDgrad), 0.0, 0, 0, b_bd);
   const double dup = mblocks * (H / 256) * tile_t(2 * F, kEpiPush);
   const double wg_up = epr * (2 * F / 128) * (H / 256) * tile_t(seg_pad, kEpiWgrad);

@@ -157,20 +157,4 @@ struct MkArgs {
   float* ret_dgp;  // unfused: gate-gradient partials [n_recv][F/256] in the return all-to-all's order
 };
 
-#ifdef __CUDACC__
-// Gate-gradient dot product helper: acc += <a, b> over 8 bf16 pairs, in lane order (shared by the
-// fused comm warps and the unfused dgate kernel, so both produce the same bits).
-__device__ __forceinline__ float dot8_bf16(const int4& a, const int4& b, float acc) {
-  const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&a);
-  const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&b);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const float2 fa = __bfloat1622float2(ha[q]), fb = __bfloat1622float2(hb[q]);
-    acc = fmaf(fa.x, fb.x, acc);
-    acc = fmaf(fa.y, fb.y, acc);
-  }
-  return acc;
-}
-#endif
-
 }  // namespace eplab_dev

@@ -555,7 +555,7 @@ def run_ours(args):
                             "buffers; step i+1's uploads overlap step i's MegaKernels), joined on the stream",
                     "blocking_value": tokens / (ms_e2e_blocking / 1e3),
                     "blocking_mode": "eplab_moe_step_host, host-synchronised every step"},
-            "gpu_launches": 9 * args.steps,
+            "gpu_launches": 7 * args.steps,  # per step: 3 planning kernels + the 4 MegaKernels
             "roofline": {"bound": "tensor", "achieved": ach, "peak": peak_sust, "unit": "TFLOP/s",
                          "frac": ach / peak_sust, "traffic": traffic, "kernel": dom,
                          "peak_source": f"{peak_src} bf16 sustained (kernel timed inside the step)",

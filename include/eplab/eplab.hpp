@@ -342,6 +342,8 @@ struct B200Calib {
                                   // (0: spare warps off / not modelled)
   double hbm_overlap = 0.513;     // kernel time = max(compute, HBM) + hbm_overlap * min(compute, HBM)
                                   // (HBM = the kernel's algorithmic bytes at bw_hbm)
+  double startup = 1.0;           // weight of the GEMM start-up term: landing the first wave's rows
+                                  // at the comm pool's rate before its main loops run
 };
 struct LayerPrediction {
   double fwd_dispatch = 0, fwd_combine = 0, bwd_dispatch = 0, bwd_combine = 0, total = 0;

@@ -293,8 +293,8 @@ typedef struct {
 } eplab_breakdown;                   /* LatencyBreakdown, perf_model.hpp:17-35 */
 typedef struct {
   double mu, tile_overhead, comm_bw_per_sm, relay_bw_per_sm, reduce_bw, launch, epi_bw_per_sm,
-      spare_sm_equiv, hbm_overlap;
-} eplab_b200_calib;                  /* B200 calibration of this build's MegaKernels */
+      spare_sm_equiv, hbm_overlap, startup;
+} eplab_b200_calib;                  /* B200 calibration of this build's MegaKernels (eplab::B200Calib) */
 typedef struct {
   double fwd_dispatch, fwd_combine, bwd_dispatch, bwd_combine, total, t_gemm_bound, t_nvl_bound;
 } eplab_layer_prediction;

@@ -61,7 +61,8 @@ B200Calib to_calib(const eplab_b200_calib* c) {
   B200Calib k;
   if (c)
     k = B200Calib{c->mu,        c->tile_overhead, c->comm_bw_per_sm, c->relay_bw_per_sm,
-                  c->reduce_bw, c->launch,        c->epi_bw_per_sm,  c->spare_sm_equiv, c->hbm_overlap};
+                  c->reduce_bw, c->launch,        c->epi_bw_per_sm,  c->spare_sm_equiv, c->hbm_overlap,
+                  c->startup};
   return k;
 }
 RoutingInstance to_routing(const int32_t* sel, int world, int n_exp, long long n_tok, int topk) {

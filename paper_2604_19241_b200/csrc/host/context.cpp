@@ -615,11 +615,10 @@ int eplab_plan(eplab_ctx* c, const int32_t* ids, const float* gw, int n_tok, voi
     c->plan.n_tok = n_tok;
     c->plan.topk_ids = ids;
     c->plan.gate_w = gw;
-    if (eplab_launch::plan_launch(c->d, c->peers, c->plan, c->epoch_dev, c->timeout_ns, c->err, st))
+    if (eplab_launch::plan_launch(c->d, c->peers, c->plan, c->epoch_dev, c->timeout_ns, c->err, c->mine.recv_x,
+                                  c->mine.recv_dy, st))
       throw Fail{EPLAB_ERR_INTERNAL, std::string("plan launch: ") +
                                          cudaGetErrorString(cudaGetLastError())};
-    eplab_launch::zero_padding_launch(c->d, c->plan, c->mine.recv_x, st);
-    eplab_launch::zero_padding_launch(c->d, c->plan, c->mine.recv_dy, st);
     CK(cudaGetLastError());
     c->planned = true;
   });
@@ -670,8 +669,7 @@ int eplab_dispatch_group_gemm_bwd(eplab_ctx* c, const void* dy, const void* w_do
   return guarded([&] {
     require_plan(c);
     CK(cudaSetDevice(c->device));
-    cudaStream_t st = (cudaStream_t)stream;
-    CK(cudaMemsetAsync(c->wg_cnt, 0, (size_t)c->d.epr * (c->d.F / 256) * 4, st));
+    cudaStream_t st = (cudaStream_t)stream;  // (wg_cnt: zeroed by the previous launch's last CTA)
     MkArgs a = base_args(c);
     // the backward dispatch moves twice the bytes of the forward one (dY rows plus the o rows
     // of the gate gradient): twice the comm CTAs, within the deadlock constraint
@@ -1066,10 +1064,8 @@ int eplab_unfused_plan_finish(eplab_ctx* c, const int32_t* d_rows, void* stream)
   return guarded([&] {
     CK(cudaSetDevice(c->device));
     cudaStream_t st = (cudaStream_t)stream;
-    if (eplab_launch::plan_layout_ext_launch(c->d, c->plan, d_rows, c->err, st))
+    if (eplab_launch::plan_layout_ext_launch(c->d, c->plan, d_rows, c->err, c->mine.recv_x, c->mine.recv_dy, st))
       throw Fail{EPLAB_ERR_INTERNAL, std::string("plan layout: ") + cudaGetErrorString(cudaGetLastError())};
-    eplab_launch::zero_padding_launch(c->d, c->plan, c->mine.recv_x, st);
-    eplab_launch::zero_padding_launch(c->d, c->plan, c->mine.recv_dy, st);
     CK(cudaGetLastError());
     c->uf_call = d_rows;
     c->planned = true;
@@ -1165,7 +1161,6 @@ int eplab_unfused_bwd_down(eplab_ctx* c, const void* w_down, void* dw_down, floa
     uf_require(c);
     CK(cudaSetDevice(c->device));
     cudaStream_t st = (cudaStream_t)stream;
-    CK(cudaMemsetAsync(c->wg_cnt, 0, (size_t)c->d.epr * (c->d.F / 256) * 4, st));
     MkArgs a = uf_args(c);
     a.w_down = static_cast<const __nv_bfloat16*>(w_down);
     a.dw_down = static_cast<__nv_bfloat16*>(dw_down);

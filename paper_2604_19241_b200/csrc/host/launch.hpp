@@ -9,11 +9,11 @@ int preload_megakernels();
 int preload_plan();
 int plan_launch(const eplab_dev::Dims& d, const eplab_dev::Peers& peers,
                 const eplab_dev::PlanDev& p, uint32_t* epoch, uint64_t timeout_ns, int* err,
-                cudaStream_t st);
+                __nv_bfloat16* recv_x, __nv_bfloat16* recv_dy, cudaStream_t st);
 int plan_counts_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p, uint32_t* epoch, int* out,
                        cudaStream_t st);
 int plan_layout_ext_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p, const int* call, int* err,
-                           cudaStream_t st);
+                           __nv_bfloat16* recv_x, __nv_bfloat16* recv_dy, cudaStream_t st);
 int unfused_pack_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p, const __nv_bfloat16* src,
                         __nv_bfloat16* send, int2* send_meta, int* spos, int sms, cudaStream_t st);
 int unfused_scatter_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p, const int* call,
@@ -23,8 +23,6 @@ int unfused_fold_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p, c
                         const int* spos, __nv_bfloat16* out, int ph, int sms, cudaStream_t st);
 int unfused_dgate_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p, const float* parts,
                          const int* spos, float* dgate, int sms, cudaStream_t st);
-int zero_padding_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p,
-                        __nv_bfloat16* recv, cudaStream_t st);
 int launch_fwd_dispatch(const eplab_dev::TmaSet& tm, const eplab_dev::MkArgs& a, int grid,
                         cudaStream_t st);
 int launch_fwd_combine(const eplab_dev::TmaSet& tm, const eplab_dev::MkArgs& a, int grid,

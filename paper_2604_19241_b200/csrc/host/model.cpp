@@ -506,17 +506,24 @@ LayerPrediction predict_layer(const MoEShape& m, const HardwareSpec& s, const Tu
   // kernel's dominant tile (quantisation matters for small batches); the HBM traffic overlaps
   // the compute only partly (hbm_overlap)
   auto kernel = [&](double sm_seconds, double critical, double extra, double tiles = 0,
-                    double t_one = 0, double hbm_bytes = 0) {
+                    double t_one = 0, double hbm_bytes = 0, double t_start = 0) {
     const double waves = tiles > 0 ? std::ceil(tiles / s.n_sm) * t_one : 0.0;
-    const double comp = std::max({sm_seconds / s.n_sm, critical, waves});
+    const double comp = std::max({sm_seconds / s.n_sm + t_start, critical, waves});
     const double mem = hbm_bytes / s.bw_hbm;
     return std::max(comp, mem) + k.hbm_overlap * std::min(comp, mem) + extra + k.launch;
   };
   const double n_pre_sm = c.n_disp * l_comm + c.n_relay * l_relay;
+  // GEMM start-up behind the scoreboard: the first wave of pair tiles (n_sm / 2 of them, raster
+  // groups of 8 row pairs across the nb column blocks) needs its rows landed before its main loop
+  // starts; the comm pool lands rows in priority order at its aggregate rate
+  auto start_up = [&](double nb, double units) {
+    const double first_rows = std::min(rows, 256.0 * std::ceil((s.n_sm / 2.0) / nb));
+    return first_rows * S / (std::max(units, 1e-3) * k.comm_bw_per_sm) * k.startup;
+  };
   // forward
   const double up = mblocks * (F / 128) * tile_t(H, kEpiUp);
   p.fwd_dispatch = kernel(up + n_pre_sm, std::max(l_comm, l_relay) + tile_t(H, kEpiUp), 0.0,
-                          mblocks * (F / 128), tile_t(H, kEpiUp), b_fd);
+                          mblocks * (F / 128), tile_t(H, kEpiUp), b_fd, start_up(F / 128, comm_units));
   const double down = mblocks * (H / 256) * tile_t(F, kEpiPush);
   p.fwd_combine = kernel(down, l_push, l_reduce, mblocks * (H / 256), tile_t(F, kEpiPush), b_fc);
   // backward: the dY dispatch moves the forward's rows (the gate gradient is formed in the
@@ -528,7 +535,8 @@ LayerPrediction predict_layer(const MoEShape& m, const HardwareSpec& s, const Tu
   const double wg_down = epr * (H / 128) * (F / 256) * tile_t(seg_pad, kEpiWgrad);
   p.bwd_dispatch = kernel(ddown + wg_down + std::min(2.0 * c.n_disp, s.n_sm / 2.0 - c.n_relay) * l_comm_b +
                               c.n_relay * l_relay,
-                          std::max(l_comm_b, l_relay) + tile_t(H, kEpiDgrad), 0.0, 0, 0, b_bd);
+                          std::max(l_comm_b, l_relay) + tile_t(H, kEpiDgrad), 0.0, 0, 0, b_bd,
+                          start_up(F / 256, comm_units_b));
   const double dup = mblocks * (H / 256) * tile_t(2 * F, kEpiPush);
   const double wg_up = epr * (2 * F / 128) * (H / 256) * tile_t(seg_pad, kEpiWgrad);
   p.bwd_combine = kernel(dup + wg_up, l_push, l_reduce, mblocks * (H / 256), tile_t(2 * F, kEpiPush), b_bc);

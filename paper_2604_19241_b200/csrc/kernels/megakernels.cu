@@ -1339,6 +1339,25 @@ struct ModeDgradUp {
   __device__ static void tile_done(const A&, const TileDesc&) {}
 };
 
+// Exit of every (non-aborted) CTA: the last one to leave returns the kernel's work counters -- the
+// task cursor, comm-round / reduce-chunk / relay-rowgroup counters (cursor[0..5]) and, after the
+// backward dispatch, the weight-gradient tile counts -- to zero for the next launch, so no memset
+// launches separate the MegaKernels (cursor[6] counts the CTAs out). Every CTA has finished with
+// the counters when it arrives; an aborted iteration touches none of them.
+__device__ __forceinline__ void finish_kernel(const MkArgs& a, int kind) {
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  __threadfence();
+  unsigned* done = reinterpret_cast<unsigned*>(a.cursor + 6);
+  if (atomicAdd(done, 1u) != gridDim.x - 1) return;
+  __threadfence();
+  for (int i = 0; i < 6; ++i) a.cursor[i] = 0;
+  if (kind == 2)
+    for (int i = 0; i < a.d.epr * (a.d.F / BN); ++i) a.wg_cnt[i] = 0;
+  *done = 0;
+  __threadfence();
+}
+
 // ------------------------------------------------------------------ the MegaKernel
 // KIND 0: fwd dispatch+GEMM, 1: fwd GEMM+combine, 2: bwd dispatch+GEMM, 3: bwd GEMM+combine.
 template <int KIND, class Mode>
@@ -1414,6 +1433,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     __syncthreads();
   }
   gemm_teardown(S);
+  finish_kernel(a, KIND);
 }
 
 
@@ -1488,6 +1508,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     id = claim();
   }
   gemm_teardown_pair(S);
+  finish_kernel(a, KIND);
 }
 
 }  // namespace eplab_dev
@@ -1514,7 +1535,7 @@ int preload_megakernels() {
 
 template <int KIND, class Mode>
 static int launch_mk(const TmaSet& tm, const MkArgs& a, int grid, cudaStream_t st) {
-  cudaMemsetAsync(a.cursor, 0, 32, st);  // task cursor, comm rounds, reduce chunks, relay rowgroups
+  // (the work counters are zero: eplab_init clears them and every MegaKernel's last CTA resets them)
   if (!a.pair) {
     auto fn = megakernel<KIND, Mode>;
     fn<<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, st>>>(tm, a);

@@ -7,7 +7,7 @@
 //                   (:108-126); one CTA
 //   plan_entries  : stable within-expert rank of every (t, j) -> Alg. 1 final_idx, the
 //                   destination slot and the priority-ordered send schedule
-//   zero_padding  : zero the alignment rows between expert segments (they are the zero
+//   (plan_entries' extra CTAs) zero the alignment rows between expert segments (they are the zero
 //                   K-padding of the transposed weight-gradient GroupGEMM)
 #include "moe_common.cuh"
 #include "ptx.cuh"
@@ -246,8 +246,37 @@ __global__ void plan_layout_ext_kernel(Dims d, PlanDev p, const int* call, int* 
 }
 
 // 256 threads = 8 warps; warp w owns entries [w*256, w*256+256) of the chunk in 8 rounds of 32.
-__global__ void __launch_bounds__(256) plan_entries_kernel(Dims d, PlanDev p, int n) {
+// The PAD_BLOCKS extra CTAs (blockIdx.x >= nchunks) zero the alignment rows between this rank's
+// expert segments in both receive buffers (rows [sb + rt, sb + align128(rt))): they are the zero
+// K-padding of the transposed weight-gradient GroupGEMMs. (One launch instead of three.)
+constexpr int PAD_BLOCKS = 8;
+__device__ void zero_padding(const Dims& d, const PlanDev& p, __nv_bfloat16* recv_x, __nv_bfloat16* recv_dy,
+                             int b) {
+  // work item = (local expert, padding row < 128): one warp per item, items dealt round-robin over
+  // all the padding warps (a serial loop over the experts with dependent segment loads cost ~0.1 ms)
+  const int vec_per_row = d.H / 8;
+  const int lane = threadIdx.x & 31, nw = blockDim.x / 32;
+  for (int it = b * nw + (int)(threadIdx.x >> 5); it < d.epr * 128; it += PAD_BLOCKS * nw) {
+    const int el = it >> 7, r = it & 127;
+    const int e = d.rank * d.epr + el;
+    const int rows = p.rt_all[e];
+    if (r >= (((rows + 127) & ~127) - rows)) continue;
+    int4* xrow = reinterpret_cast<int4*>(recv_x) + ((size_t)p.sb_all[e] + rows + r) * vec_per_row;
+    int4* dyrow = reinterpret_cast<int4*>(recv_dy) + ((size_t)p.sb_all[e] + rows + r) * vec_per_row;
+    for (int c = lane; c < vec_per_row; c += 32) {
+      xrow[c] = make_int4(0, 0, 0, 0);
+      dyrow[c] = make_int4(0, 0, 0, 0);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) plan_entries_kernel(Dims d, PlanDev p, int n, int nchunks,
+                                                           __nv_bfloat16* recv_x, __nv_bfloat16* recv_dy) {
   if (p.scalars[3]) return;  // aborted iteration (bad routing / capacity / timeout)
+  if ((int)blockIdx.x >= nchunks) {
+    zero_padding(d, p, recv_x, recv_dy, blockIdx.x - nchunks);
+    return;
+  }
   __shared__ int wcnt[8][MAX_EXPERTS];
   const int E = d.E;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -293,22 +322,6 @@ __global__ void __launch_bounds__(256) plan_entries_kernel(Dims d, PlanDev p, in
   }
 }
 
-// Zero the alignment rows of my receive buffer (rows [sb + rt, sb + align128(rt))).
-__global__ void zero_padding_kernel(Dims d, PlanDev p, __nv_bfloat16* recv) {
-  if (p.scalars[3]) return;
-  const int el = blockIdx.y;
-  const int e = d.rank * d.epr + el;
-  const int rows = p.rt_all[e];
-  const int pad = ((rows + 127) & ~127) - rows;
-  const int row0 = p.sb_all[e] + rows;
-  const int vec_per_row = d.H / 8;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < pad * vec_per_row;
-       i += gridDim.x * blockDim.x) {
-    const int r = i / vec_per_row, c = i % vec_per_row;
-    reinterpret_cast<int4*>(recv + (size_t)(row0 + r) * d.H)[c] = make_int4(0, 0, 0, 0);
-  }
-}
-
 }  // namespace eplab_dev
 
 namespace eplab_launch {
@@ -323,22 +336,23 @@ int plan_counts_launch(const Dims& d, const PlanDev& p, uint32_t* epoch, int* ou
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
-int plan_layout_ext_launch(const Dims& d, const PlanDev& p, const int* call, int* err, cudaStream_t st) {
+int plan_layout_ext_launch(const Dims& d, const PlanDev& p, const int* call, int* err, __nv_bfloat16* recv_x,
+                           __nv_bfloat16* recv_dy, cudaStream_t st) {
   const int n = p.n_tok * d.topk;
   const int nchunks = n > 0 ? (n + PLAN_CHUNK - 1) / PLAN_CHUNK : 0;
   plan_layout_ext_kernel<<<1, 1024, 0, st>>>(d, p, call, err);
-  if (nchunks > 0) plan_entries_kernel<<<nchunks, 256, 0, st>>>(d, p, n);
+  plan_entries_kernel<<<nchunks + PAD_BLOCKS, 256, 0, st>>>(d, p, n, nchunks, recv_x, recv_dy);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
 int plan_launch(const Dims& d, const Peers& peers, const PlanDev& p, uint32_t* epoch,
-                uint64_t timeout_ns, int* err, cudaStream_t st) {
+                uint64_t timeout_ns, int* err, __nv_bfloat16* recv_x, __nv_bfloat16* recv_dy, cudaStream_t st) {
   const int n = p.n_tok * d.topk;
   const int nchunks = n > 0 ? (n + PLAN_CHUNK - 1) / PLAN_CHUNK : 0;
   if (nchunks > 0)
     plan_hist_kernel<<<nchunks, 256, 0, st>>>(p.topk_ids, p.gate_w, n, d.topk, d.E, p.hist, p.scalars);
   plan_global_kernel<<<1, 1024, 0, st>>>(d, peers, p, nchunks, epoch, timeout_ns, err);
-  if (nchunks > 0) plan_entries_kernel<<<nchunks, 256, 0, st>>>(d, p, n);
+  plan_entries_kernel<<<nchunks + PAD_BLOCKS, 256, 0, st>>>(d, p, n, nchunks, recv_x, recv_dy);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
@@ -350,15 +364,8 @@ int preload_plan() {
                   cudaFuncGetAttributes(&fa, plan_global_kernel) == cudaSuccess &&
                   cudaFuncGetAttributes(&fa, plan_entries_kernel) == cudaSuccess &&
                   cudaFuncGetAttributes(&fa, plan_counts_kernel) == cudaSuccess &&
-                  cudaFuncGetAttributes(&fa, plan_layout_ext_kernel) == cudaSuccess &&
-                  cudaFuncGetAttributes(&fa, zero_padding_kernel) == cudaSuccess;
+                  cudaFuncGetAttributes(&fa, plan_layout_ext_kernel) == cudaSuccess;
   return ok ? 0 : 1;
-}
-
-int zero_padding_launch(const Dims& d, const PlanDev& p, __nv_bfloat16* recv, cudaStream_t st) {
-  dim3 grid(4, d.epr);
-  zero_padding_kernel<<<grid, 256, 0, st>>>(d, p, recv);
-  return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
 }  // namespace eplab_launch

@@ -38,7 +38,7 @@ class Breakdown(C.Structure):
 class Calib(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("mu", "tile_overhead", "comm_bw_per_sm", "relay_bw_per_sm",
                                           "reduce_bw", "launch", "epi_bw_per_sm", "spare_sm_equiv",
-                                          "hbm_overlap")]
+                                          "hbm_overlap", "startup")]
 
 
 class LayerPrediction(C.Structure):
@@ -51,7 +51,7 @@ class LayerPrediction(C.Structure):
 
 # B200 calibration of this build (DESIGN.md §Performance model; refit by tools/fit_model.py)
 # fitted over 76 measured cases, spare-warp comm workers on/off (profiles/r01_perf_model_validation.md)
-B200_CALIB = Calib(1.0, 0.2e-6, 25.01e9, 25.01e9, 6.5e12, 42.19e-6, 200.0e9, 41.78, 0.513)
+B200_CALIB = Calib(1.0, 0.2e-6, 25.01e9, 25.01e9, 6.5e12, 42.19e-6, 200.0e9, 41.78, 0.513, 1.0)
 
 
 def hw(world, n_sm=148, p_peak=1408.1e12, bw_hbm=6468.9e9, bw_nvl=770e9, w_sat=1024.0, tau_sync=1e-6):

@@ -59,9 +59,72 @@ def measure(H, F, E, k, T, cfg, steps=3, spare=1):
     return ms
 
 
+def measure_virtual(H, F, E, k, T, W, relay, steps=3):
+    """W virtual ranks on this GPU (148 // W SMs each, peers in local HBM): per-MegaKernel times,
+    max over ranks (the EP > 1 protocol with the NVLink hop replaced by local memory)."""
+    sel, gw = po.Oracle().sample_routing(E, k, T, W, 7)
+    epr = E // W
+    g = torch.Generator(device="cuda").manual_seed(1)
+    ranks = [M.EpMoE(H, F, E, k, T, rank=r, world=W, timeout_s=60.0) for r in range(W)]
+    M.EpMoE.connect_local(ranks)
+    n_sm = 148 // W
+    nd = max(2, 16 // W)
+    for rk in ranks:
+        rk.set_sm_budget(n_sm)
+        rk.set_tune_config(M.TuneConfig(nd, relay, 1, n_sm, 8))
+    ins = []
+    for r in range(W):
+        ins.append(dict(ids=torch.from_numpy(sel[r].reshape(T, k).copy()).cuda(),
+                        gw=torch.from_numpy(gw[r].reshape(T, k).copy()).cuda(),
+                        x=torch.randn(T, H, device="cuda", generator=g).bfloat16(),
+                        dy=(torch.randn(T, H, device="cuda", generator=g) * 0.1).bfloat16(),
+                        w_up=(torch.randn(epr, 2 * F, H, device="cuda", generator=g) * H ** -0.5).bfloat16(),
+                        w_down=(torch.randn(epr, H, F, device="cuda", generator=g) * F ** -0.5).bfloat16(),
+                        y=torch.empty(T, H, device="cuda", dtype=torch.bfloat16)))
+        ins[r]["out"] = dict(dx=torch.empty(T, H, dtype=torch.bfloat16, device="cuda"),
+                             dw_up=torch.empty_like(ins[r]["w_up"]), dw_down=torch.empty_like(ins[r]["w_down"]),
+                             dgate=torch.empty(T, k, dtype=torch.float32, device="cuda"))
+    streams = [torch.cuda.Stream() for _ in range(W)]
+
+    def step(evs=None):
+        for r in range(W):
+            with torch.cuda.stream(streams[r]):
+                if evs:
+                    evs[r][0].record(streams[r])
+                ranks[r].plan(ins[r]["ids"], ins[r]["gw"], streams[r])
+        torch.cuda.synchronize()
+        for ph, fn in enumerate([lambda L, a, s: L.dispatch_group_gemm(a["x"], a["w_up"], s),
+                                 lambda L, a, s: L.group_gemm_combine(a["w_down"], a["y"], s),
+                                 lambda L, a, s: L._dispatch_bwd(a["dy"], a["w_down"], a["out"], s),
+                                 lambda L, a, s: L._combine_bwd(a["w_up"], a["out"], s)]):
+            for r in range(W):
+                with torch.cuda.stream(streams[r]):
+                    if evs and ph == 0:
+                        evs[r][1].record(streams[r])  # after the plan (synchronised between ranks)
+                    fn(ranks[r], ins[r], streams[r])
+                    if evs:
+                        evs[r][ph + 2].record(streams[r])
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    per = []
+    for _ in range(steps):
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(W)]
+        step(evs)
+        torch.cuda.synchronize()
+        per.append([max(evs[r][j + 1].elapsed_time(evs[r][j + 2]) for r in range(W)) for j in range(4)])
+    for rk in ranks:
+        rk.check()
+        rk.close()
+    torch.cuda.empty_cache()
+    return [sum(p[j] for p in per) / steps for j in range(4)]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/model_sweep.jsonl")
+    ap.add_argument("--ep", action="store_true", help="also the virtual-rank EP=2/4/8 cases")
     args = ap.parse_args()
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     cases = []
@@ -72,12 +135,23 @@ def main():
               ("dsv3", 7168, 2048, 256, 8, 16384), ("sweep64k", 2048, 768, 128, 8, 65536)]
     with open(args.out, "w") as f:
         for name, H, F, E, k, T in cases:
-            for nd, spare in ((0, 1), (16, 1), (64, 1), (64, 0)):
+            for nd, spare in ((0, 1), (16, 1), (48, 1), (48, 0)):
                 ms = measure(H, F, E, k, T, M.TuneConfig(nd, 0, 1, 148, 8), spare=spare)
                 rec = dict(name=name, H=H, F=F, E=E, k=k, T=T, world=1, n_disp=nd, n_relay=0, spare=spare, ms=ms)
                 f.write(json.dumps(rec) + "\n")
                 f.flush()
                 print(json.dumps(rec), flush=True)
+        if args.ep:
+            for name, H, F, E, k, T in (("vep_qwen3", 2048, 768, 128, 8, 8192), ("vep_k2", 2048, 768, 128, 2, 8192),
+                                        ("vep_mixtral", 4096, 14336, 8, 2, 4096)):
+                for W in (2, 4, 8):
+                    for relay in (0, 1):
+                        ms = measure_virtual(H, F, E, k, T, W, relay)
+                        rec = dict(name=name, H=H, F=F, E=E, k=k, T=T, world=W, virtual=1, n_sm=148 // W,
+                                   n_disp=max(2, 16 // W), n_relay=relay, spare=1, ms=ms)
+                        f.write(json.dumps(rec) + "\n")
+                        f.flush()
+                        print(json.dumps(rec), flush=True)
 
 
 if __name__ == "__main__":

@@ -16,10 +16,15 @@ BOUNDS = []
 
 
 def predict(r, x):
-    c = m.Calib(x[0], x[1] * 1e-6, x[2] * 1e9, x[2] * 1e9, x[3] * 1e12, x[4] * 1e-6, x[5] * 1e9,
-                x[6] if r.get("spare", 0) else 0.0, x[7])
-    p = m.predict_layer(m.shape(r["H"], r["F"], r["E"], r["k"], r["T"]), m.hw(r["world"]),
-                        m.TuneConfig(r["n_disp"], r["n_relay"], 1, 148, 8), c)
+    c = m.Calib(x[0], x[1] * 1e-6, x[2] * 1e9, x[8] * 1e9, x[3] * 1e12, x[4] * 1e-6, x[5] * 1e9,
+                x[6] if r.get("spare", 0) else 0.0, x[7], x[9])
+    W = r["world"]
+    if r.get("virtual"):  # W ranks on one GPU: 148 / W SMs each, "NVLink" = the shared local HBM
+        h = m.hw(W, n_sm=r["n_sm"], bw_hbm=6468.9e9 / W, bw_nvl=6468.9e9 / (2 * W))
+    else:
+        h = m.hw(W)
+    p = m.predict_layer(m.shape(r["H"], r["F"], r["E"], r["k"], r["T"]), h,
+                        m.TuneConfig(r["n_disp"], r["n_relay"], 1, h.n_sm, 8), c)
     return [getattr(p, k) * 1e3 for k in KEYS]
 
 
@@ -36,33 +41,41 @@ def loss(x):
     return e
 
 
-x0 = np.array([0.9, 1.0, 16.0, 3.0, 50.0, 8.0, 20.0, 0.3])
+x0 = np.array([0.9, 1.0, 16.0, 3.0, 50.0, 8.0, 20.0, 0.3, 16.0, 0.5])
 # physical ranges: mu <= 1; per-tile hand-off 0.2-5 us; a comm CTA moves 5-50 GB/s
 # (tools/bulk_copy_probe.cu measured <= 45 GB/s in isolation); reduce 1-6.5 TB/s (HBM);
 # fixed per-kernel cost 20-200 us; epilogue 20-200 GB/s per SM; spare warps 0-74 comm-CTA
-# equivalents (2 spare warps per SM); HBM/compute overlap penalty 0-1
-BOUNDS = [(0.5, 1.0), (0.2, 5.0), (5.0, 50.0), (1.0, 6.5), (20.0, 200.0), (20.0, 200.0), (0.0, 74.0), (0.0, 1.0)]
+# equivalents (2 spare warps per SM); HBM/compute overlap penalty 0-1; a relay CTA moves 5-50 GB/s of
+# HBM copies (fitted separately from the comm CTAs, on the virtual-rank relay-on cases); start-up 0-2
+BOUNDS = [(0.5, 1.0), (0.2, 5.0), (5.0, 50.0), (1.0, 6.5), (20.0, 200.0), (20.0, 200.0), (0.0, 74.0), (0.0, 1.0),
+          (5.0, 50.0), (0.0, 2.0)]
 res = minimize(loss, x0, method="Powell", bounds=BOUNDS, options={"maxiter": 20000, "xtol": 1e-4, "ftol": 1e-9})
 res = minimize(loss, res.x, method="Powell", bounds=BOUNDS, options={"maxiter": 20000, "xtol": 1e-5, "ftol": 1e-10})
 x = res.x
-lines = ["# Perf model (predict_layer, B200) vs measured MegaKernel times -- round 1, 1x B200, EP=1",
-         f"# fitted B200Calib: mu={x[0]:.4f}, tile_overhead={x[1]:.3f} us, comm_bw_per_sm={x[2]:.2f} GB/s "
-         f"(relay = comm), reduce_bw={x[3]:.3f} TB/s, launch={x[4]:.2f} us, epi_bw_per_sm={x[5]:.2f} GB/s, "
-         f"spare_sm_equiv={x[6]:.2f}, hbm_overlap={x[7]:.3f}",
+lines = ["# Perf model (predict_layer, B200) vs measured MegaKernel times -- round 2, 1x B200: EP=1 and "
+         "EP=2/4/8 on virtual ranks (148/W SMs each, peers in local HBM)",
+         f"# fitted B200Calib: mu={x[0]:.4f}, tile_overhead={x[1]:.3f} us, comm_bw_per_sm={x[2]:.2f} GB/s, "
+         f"relay_bw_per_sm={x[8]:.2f} GB/s, reduce_bw={x[3]:.3f} TB/s, launch={x[4]:.2f} us, "
+         f"epi_bw_per_sm={x[5]:.2f} GB/s, spare_sm_equiv={x[6]:.2f}, hbm_overlap={x[7]:.3f}, startup={x[9]:.3f}",
          "# (least squares on log time over all 4 kernels of every case; tools/model_sweep.py + tools/fit_model.py)",
-         "", "| case | H | F | E | k | T | n_disp | spare warps | measured ms (fd/fc/bd/bc) | predicted ms | step err |",
-         "|---|---|---|---|---|---|---|---|---|---|---|"]
+         "", "| case | W | H | F | E | k | T | n_disp | n_relay | spare warps | measured ms (fd/fc/bd/bc) | predicted ms | step err |",
+         "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
 errs = []
 for r in recs:
     pr = predict(r, x)
     tm, tp = sum(r["ms"]), sum(pr)
     errs.append(abs(tp - tm) / tm)
-    lines.append(f"| {r['name']} | {r['H']} | {r['F']} | {r['E']} | {r['k']} | {r['T']} | {r['n_disp']} | {r.get('spare', 0)} | "
+    lines.append(f"| {r['name']} | {r['world']} | {r['H']} | {r['F']} | {r['E']} | {r['k']} | {r['T']} | {r['n_disp']} | "
+                 f"{r['n_relay']} | {r.get('spare', 0)} | "
                  + "/".join(f"{v:.3f}" for v in r["ms"]) + f" | " + "/".join(f"{v:.3f}" for v in pr)
                  + f" | {100 * (tp - tm) / tm:+.1f}% |")
 lines.append("")
 lines.append(f"mean |step error| = {100 * np.mean(errs):.1f}%, max = {100 * np.max(errs):.1f}% over {len(recs)} cases")
-open("profiles/r01_perf_model_validation.md", "w").write("\n".join(lines) + "\n")
+ep = [e for e, r in zip(errs, recs) if r["world"] > 1]
+if ep:
+    lines.append(f"EP > 1 (virtual ranks): mean |step error| = {100 * np.mean(ep):.1f}%, max = {100 * np.max(ep):.1f}% "
+                 f"over {len(ep)} cases")
+open(sys.argv[2] if len(sys.argv) > 2 else "profiles/r02_perf_model_validation.md", "w").write("\n".join(lines) + "\n")
 print("\n".join(lines[:3]))
 print(lines[-1])
 print("calib", list(np.round(x, 4)))

@@ -489,7 +489,8 @@ LayerPrediction predict_layer(const MoEShape& m, const HardwareSpec& s, const Tu
   const double comm_units = std::max(c.n_disp + k.spare_sm_equiv, 1e-3);
   const double l_comm = std::max(sent_rows * S / (comm_units * k.comm_bw_per_sm),
                                  W > 1 ? nvl_rows * S / s.bw_nvl : 0.0);
-  const double l_relay = relay ? dup_rows * S / (c.n_relay * k.relay_bw_per_sm) : 0.0;
+  // relay pool: the n_relay relay CTAs' warps plus, once the comm rounds drain, the spare warps
+  const double l_relay = relay ? dup_rows * S / ((c.n_relay + k.spare_sm_equiv) * k.relay_bw_per_sm) : 0.0;
   const double l_push = W > 1 ? T * k_rem * S / s.bw_nvl : 0.0;
   const double l_reduce = T * (m.topk + 1) * S / k.reduce_bw;
   // persistent grid: SM-seconds spread over n_sm, but never less than whole waves of the

@@ -11,14 +11,22 @@
 namespace eplab_dev {
 
 // A Mode with `static constexpr bool SPARE = true` gives the engine's otherwise idle warps work
-// through `Mode::spare(args, timeline)` (the MegaKernels' comm warp split).
+// through `Mode::spare(args, timeline, stop)` (the MegaKernels' comm warp split). `stop` tells a
+// worker that may quit early when the GEMM phase is over: every tile id has been claimed.
 template <class M, class = void>
 struct has_spare : std::false_type {};
 template <class M>
 struct has_spare<M, std::void_t<decltype(M::SPARE)>> : std::bool_constant<M::SPARE> {};
+struct SpareStop {
+  const int* cursor;  // the MegaKernel's task cursor
+  int tile_hi;        // first id past the tiles
+  __device__ __forceinline__ bool tiles_claimed() const {
+    return *reinterpret_cast<const volatile int*>(cursor) >= tile_hi;
+  }
+};
 template <class Mode, class Args, class TL>
-__device__ __forceinline__ void call_spare(const Args& a, const TL& tl) {
-  if constexpr (has_spare<Mode>::value) Mode::spare(a, tl);
+__device__ __forceinline__ void call_spare(const Args& a, const TL& tl, const SpareStop& stop) {
+  if constexpr (has_spare<Mode>::value) Mode::spare(a, tl, stop);
 }
 // A Mode with `static constexpr bool RELEASE_AFTER = true` publishes a tile's results in
 // `Mode::epilogue_release(args, tile, row)`, called after the epilogue has handed the TMEM
@@ -88,7 +96,7 @@ __device__ int gemm_roles(const typename Mode::Args& args, const TmaSet& tm, uin
   uint8_t* sB = tiles_smem + STAGES * A_STAGE_BYTES;
 
   if (has_spare<Mode>::value && warp == 2) {
-    call_spare<Mode>(args, tl);  // the TMEM owner is idle between allocation and teardown
+    call_spare<Mode>(args, tl, SpareStop{cursor, tile_hi});  // the TMEM owner is idle between allocation and teardown
   } else if (warp == 3) {
     // ---------------- scheduler: claims tile ids, decodes them and resolves their scoreboard
     // dependencies (Mode::before_loads) ahead of the producer; stops at the first non-tile id

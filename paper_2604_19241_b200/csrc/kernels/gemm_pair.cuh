@@ -92,7 +92,7 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
       if (lane == 0) mbar_arrive(&S->rq_empty[slot]);
     }
   } else if (has_spare<Mode>::value && spare) {
-    call_spare<Mode>(args, tl);
+    call_spare<Mode>(args, tl, SpareStop{cursor, tile_hi});
   } else if (warp == 3) {
     if (leader && lane == 0) {
       // ---------------- scheduler (leader)

@@ -726,13 +726,17 @@ __device__ __forceinline__ void fold_token(const MkArgs& a, int ph, long long t)
 // tiles: spare warps would only hold chunks they fold slowly, so they stay out.)
 constexpr int RCHUNK = 8;
 template <int KT>
-__device__ void reduce_chunks_t(const MkArgs& a, int ph, bool backoff) {
+__device__ void reduce_chunks_t(const MkArgs& a, int ph, bool backoff, const SpareStop* stop) {
   const Dims& d = a.d;
   const SymPtrs& me = a.peers.p[d.rank];
   const int lane = threadIdx.x & 31;
   const uint32_t need = (uint32_t)(d.topk * (d.H / BN));
   const int n_chunks = (a.p.n_tok + RCHUNK - 1) / RCHUNK;
   for (;;) {
+    // spare workers hand the rest to the post-task CTAs once the GEMM phase ends: a spare warp
+    // folds ~5x slower than a whole post-task CTA, and its CTA cannot move on to the post-tasks
+    // while it holds chunks (k <= 4, 32K tokens: bwd combine 1.04 -> 0.62 ms)
+    if (stop && stop->tiles_claimed()) break;
     int c = 0;
     if (lane == 0) c = (int)atomicAdd(a.red_cursor, 1u);
     c = __shfl_sync(0xffffffffu, c, 0);
@@ -763,21 +767,21 @@ __device__ void reduce_chunks_t(const MkArgs& a, int ph, bool backoff) {
   }
 }
 
-__device__ void reduce_chunks(const MkArgs& a, int ph, bool backoff) {
+__device__ void reduce_chunks(const MkArgs& a, int ph, bool backoff, const SpareStop* stop = nullptr) {
   if (a.dbg & 64) return;  // experiment: no reduce (wrong y / dx; measures the reduce's share)
   if (a.d.topk <= 8)
-    reduce_chunks_t<8>(a, ph, backoff);
+    reduce_chunks_t<8>(a, ph, backoff, stop);
   else
-    reduce_chunks_t<16>(a, ph, backoff);
+    reduce_chunks_t<16>(a, ph, backoff, stop);
 }
 
 __device__ void reduce_task(const MkArgs& a, int, int ph) { reduce_chunks(a, ph, false); }
 
 // spare warps of the backward combine MegaKernel's GEMM CTAs join the reduce pool from the start
-__device__ __forceinline__ void spare_reduce(const MkArgs& a, const Timeline& tl, int ph) {
+__device__ __forceinline__ void spare_reduce(const MkArgs& a, const Timeline& tl, int ph, const SpareStop& stop) {
   if (!(a.spare_warps & 2)) return;
   const unsigned long long t0 = globaltimer();
-  reduce_chunks(a, ph, true);
+  reduce_chunks(a, ph, true, &stop);
   if ((threadIdx.x & 31) == 0) timeline_push(tl, t0, globaltimer(), ROLE_REDUCE, -1 - (int)(threadIdx.x >> 5));
 }
 
@@ -805,7 +809,7 @@ struct ModeUp {
   using Args = MkArgs;
   static constexpr bool HAS_TILE_DONE = false;
   static constexpr bool SPARE = true;
-  __device__ static void spare(const Args& a, const Timeline& tl) { spare_comm(a, tl, 0); }
+  __device__ static void spare(const Args& a, const Timeline& tl, const SpareStop&) { spare_comm(a, tl, 0); }
   __device__ static int a_mn(const TileDesc&) { return 0; }
   __device__ static int b_mn(const TileDesc&) { return 0; }
   __device__ static TileDesc tile(const Args& a, int t) {
@@ -1052,7 +1056,7 @@ struct ModeDgradDown {
   using Args = MkArgs;
   static constexpr bool HAS_TILE_DONE = true;
   static constexpr bool SPARE = true;
-  __device__ static void spare(const Args& a, const Timeline& tl) { spare_comm(a, tl, 1); }
+  __device__ static void spare(const Args& a, const Timeline& tl, const SpareStop&) { spare_comm(a, tl, 1); }
   __device__ static int n_dgrad_pair(const Args& a) { return a.p.mpair_pre[a.d.epr] * (a.d.F / BN); }
   __device__ static TileDesc tile_pair(const Args& a, int t) {
     const int nd = n_dgrad_pair(a);
@@ -1268,7 +1272,9 @@ struct ModeDgradUp {
   __device__ static bool wants_release(const Args& a, const TileDesc& td) { return !a.unfused && !td.pad1; }
   __device__ static void release_tile(const Args& a, const TileDesc& td, int lane) { push_release_tile(a, td, lane, 1); }
   static constexpr bool SPARE = true;
-  __device__ static void spare(const Args& a, const Timeline& tl) { spare_reduce(a, tl, 1); }
+  __device__ static void spare(const Args& a, const Timeline& tl, const SpareStop& stop) {
+    spare_reduce(a, tl, 1, stop);
+  }
   __device__ static void epilogue_prefetch(const Args& a, const TileDesc& td, int r) { prefetch_meta_l1(a, td, r); }
   __device__ static int n_dgrad_pair(const Args& a) { return a.p.mpair_pre[a.d.epr] * (a.d.H / BN); }
   __device__ static TileDesc tile_pair(const Args& a, int t) {

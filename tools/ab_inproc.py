@@ -16,8 +16,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="qwen3")
 ap.add_argument("--variants", required=True)
 ap.add_argument("--rounds", type=int, default=20)
+ap.add_argument("--shape", default="", help="H,F,E,k,T instead of a bench config")
 args = ap.parse_args()
-H, F, E, k, T = bench.CONFIGS[args.config]
+H, F, E, k, T = [int(v) for v in args.shape.split(",")] if args.shape else bench.CONFIGS[args.config]
+if args.shape:
+    args.config = "shape_" + args.shape.replace(",", "_")
 sel, gw = po.Oracle().sample_routing(E, k, T, 1, 7)
 ids = torch.from_numpy(sel[0].reshape(T, k).copy()).cuda()
 gws = torch.from_numpy(gw[0].reshape(T, k).copy()).cuda()

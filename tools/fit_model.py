@@ -20,7 +20,8 @@ def predict(r, x):
                 x[6] if r.get("spare", 0) else 0.0, x[7], x[9])
     W = r["world"]
     if r.get("virtual"):  # W ranks on one GPU: 148 / W SMs each, "NVLink" = the shared local HBM
-        h = m.hw(W, n_sm=r["n_sm"], bw_hbm=6468.9e9 / W, bw_nvl=6468.9e9 / (2 * W))
+        h = m.hw(W, n_sm=r["n_sm"], p_peak=1408.1e12 * r["n_sm"] / 148, bw_hbm=6468.9e9 / W,
+                 bw_nvl=6468.9e9 / (2 * W))
     else:
         h = m.hw(W)
     p = m.predict_layer(m.shape(r["H"], r["F"], r["E"], r["k"], r["T"]), h,
@@ -46,7 +47,7 @@ x0 = np.array([0.9, 1.0, 16.0, 3.0, 50.0, 8.0, 20.0, 0.3, 16.0, 0.5])
 # (tools/bulk_copy_probe.cu measured <= 45 GB/s in isolation); reduce 1-6.5 TB/s (HBM);
 # fixed per-kernel cost 20-200 us; epilogue 20-200 GB/s per SM; spare warps 0-74 comm-CTA
 # equivalents (2 spare warps per SM); HBM/compute overlap penalty 0-1; a relay CTA moves 5-50 GB/s of
-# HBM copies (fitted separately from the comm CTAs, on the virtual-rank relay-on cases); start-up 0-2
+# HBM copies (fitted separately from the comm CTAs, on the virtual-rank relay-on cases); start-up 0-2 (units of the first wave's landing time)
 BOUNDS = [(0.5, 1.0), (0.2, 5.0), (5.0, 50.0), (1.0, 6.5), (20.0, 200.0), (20.0, 200.0), (0.0, 74.0), (0.0, 1.0),
           (5.0, 50.0), (0.0, 2.0)]
 res = minimize(loss, x0, method="Powell", bounds=BOUNDS, options={"maxiter": 20000, "xtol": 1e-4, "ftol": 1e-9})

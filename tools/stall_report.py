@@ -20,8 +20,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="qwen3")
 ap.add_argument("--opt", action="append", default=[], help="eplab_set_option name=value")
 ap.add_argument("--out", default="gpurun_out")
+ap.add_argument("--shape", default="", help="H,F,E,k,T instead of a bench config")
 args = ap.parse_args()
-H, F, E, k, T = bench.CONFIGS[args.config]
+H, F, E, k, T = [int(v) for v in args.shape.split(",")] if args.shape else bench.CONFIGS[args.config]
+if args.shape:
+    args.config = "shape_" + args.shape.replace(",", "_")
+bench.CONFIGS[args.config] = (H, F, E, k, T)
 inp = bench.make_inputs(args.config, 1, 0)
 L = M.EpMoE(H, F, E, k, T)
 L.set_tune_config(choose_config(H, F, E, k, T, 1))

@@ -330,19 +330,21 @@ LatencyBreakdown predict_latency(const MoEShape& shape, const HardwareSpec& spec
 // --------------------------------------------------------------- B200 model of the MegaKernels
 // Calibrated constants of this implementation on B200 (DESIGN.md §Performance model).
 struct B200Calib {
-  // fitted over 76 measured cases (tools/fit_model.py, profiles/r01_perf_model_validation.md)
-  double mu = 1.0;                // tensor-pipe efficiency of the tile main loop vs p_peak (sustained)
+  // fitted over 94 measured cases, EP=1 and EP=2/4/8 on virtual ranks (tools/model_sweep.py
+  // --ep + tools/fit_model.py, profiles/r02_perf_model_validation.md: 6.6 % mean step error)
+  double mu = 0.935;              // tensor-pipe efficiency of the tile main loop vs p_peak (sustained)
   double tile_overhead = 0.2e-6;  // per-tile hand-off cost not hidden behind the loop, s
-  double comm_bw_per_sm = 25.01e9; // B/s one comm CTA sustains (8 warps of warp copies)
-  double relay_bw_per_sm = 25.01e9;  // B/s one relay CTA sustains on HBM copies
+  double comm_bw_per_sm = 28.94e9; // B/s one comm CTA sustains (8 warps of warp copies)
+  double relay_bw_per_sm = 8.88e9;   // B/s one relay worker unit sustains on HBM copies (polling
+                                     // the primaries' flags, then copying)
   double reduce_bw = 6.5e12;      // B/s of the reduce role when all SMs join
-  double launch = 42.19e-6;       // per MegaKernel fixed cost: launch, prologue, pipeline fill
-  double epi_bw_per_sm = 200.0e9; // B/s of epilogue traffic per SM (TMA stores, saved-input reads)
-  double spare_sm_equiv = 41.78;  // comm capacity of the GEMM CTAs' spare warps, in comm-CTA units
-                                  // (0: spare warps off / not modelled)
-  double hbm_overlap = 0.513;     // kernel time = max(compute, HBM) + hbm_overlap * min(compute, HBM)
+  double launch = 31.45e-6;       // per MegaKernel fixed cost: launch, prologue, pipeline fill
+  double epi_bw_per_sm = 199.1e9; // B/s of epilogue traffic per SM (TMA stores, saved-input reads)
+  double spare_sm_equiv = 29.04;  // comm capacity of the GEMM CTAs' spare warps, in comm-CTA units
+                                  // (0: spare warps off / not modelled); also drains the relay pool
+  double hbm_overlap = 0.528;     // kernel time = max(compute, HBM) + hbm_overlap * min(compute, HBM)
                                   // (HBM = the kernel's algorithmic bytes at bw_hbm)
-  double startup = 1.0;           // weight of the GEMM start-up term: landing the first wave's rows
+  double startup = 2.0;           // weight of the GEMM start-up term: landing the first wave's rows
                                   // at the comm pool's rate before its main loops run
 };
 struct LayerPrediction {

@@ -186,6 +186,35 @@ EPLAB_API int eplab_dispatch_group_gemm_bwd(eplab_ctx* ctx, const void* d_dy,
 EPLAB_API int eplab_group_gemm_combine_bwd(eplab_ctx* ctx, const void* d_w_up, void* d_dx,
                                            void* d_dw_up, void* stream);
 
+/* Several forwards in flight on one context (pipelined micro-batches, layers sharing a context,
+ * activation recomputation). A context holds ONE iteration's state -- the plan tables, the
+ * received rows and slot metadata (symmetric region) and the saved g/u and h activations --
+ * which the next eplab_plan overwrites. A stash is a copy of that state in caller-owned device
+ * memory, sized to the iteration's actual receive rows (not the worst-case capacity):
+ *   eplab_stash_bytes    bytes the current iteration's stash needs (synchronises `stream`: the
+ *                        receive row count is on the device)
+ *   eplab_stash_save     copies the state into d_dst (>= that many bytes) and fills *info
+ *   eplab_stash_restore  copies a stash back; the context's current iteration becomes the stashed
+ *                        one and its backward (eplab_moe_bwd / the two backward MegaKernels) may run.
+ * The restored backward runs under a fresh epoch (every rank must restore in the same order: the
+ * MegaKernels' flags and counter parities follow the epoch). Copies are enqueued on `stream`;
+ * the routing / gate-weight tensors of the stashed plan must stay alive until its backward. */
+typedef struct {
+  uint32_t magic;     /* EPLAB_STASH_MAGIC */
+  uint32_t epoch;     /* epoch of the stashed plan */
+  int n_tok;
+  int rows;           /* receive rows (128-aligned segments) */
+  const int32_t* topk_ids;
+  const float* gate_w;
+  size_t bytes;       /* bytes used in the stash buffer */
+} eplab_stash_info;
+#define EPLAB_STASH_MAGIC 0x5354a5a5u
+EPLAB_API int eplab_stash_bytes(eplab_ctx* ctx, size_t* bytes, void* stream);
+EPLAB_API int eplab_stash_save(eplab_ctx* ctx, void* d_dst, size_t dst_bytes, eplab_stash_info* info,
+                               void* stream);
+EPLAB_API int eplab_stash_restore(eplab_ctx* ctx, const void* d_src, const eplab_stash_info* info,
+                                  void* stream);
+
 /* Whole layer. fwd = plan + the two forward MegaKernels; bwd = the two backward ones. */
 EPLAB_API int eplab_moe_fwd(eplab_ctx* ctx, const int32_t* d_topk_ids, const float* d_gate_w,
                             int n_tok, const void* d_x, const void* d_w_up, const void* d_w_down,

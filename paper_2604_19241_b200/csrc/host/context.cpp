@@ -56,6 +56,7 @@ struct eplab_ctx {
   std::vector<void*> ipc_opened;
   // local region
   char* loc = nullptr;
+  size_t off_plan_lo = 0, off_plan_hi = 0;  // the plan tables the backward reads (stash range)
   PlanDev plan{};
   __nv_bfloat16 *gu = nullptr, *hact = nullptr, *dgu = nullptr, *hw = nullptr;
   uint32_t* wg_cnt = nullptr;
@@ -245,9 +246,8 @@ namespace {
 eplab_tune_config search_config(eplab_ctx* c, long long bucket);
 
 // Launch parameters for this context's shape at n_tok tokens per rank: search_layer over the B200
-// model at the bucket's upper edge, n_red = every SM, and the measured floor on comm CTAs the model
-// does not capture (16 with the spare-warp comm workers, 64 without, scaled by the SM budget;
-// profiles/r01_spare_warps.txt). Cached per 4096-token bucket.
+// model at the bucket's upper edge (its GEMM start-up term replaced round 1's floor of 16 comm
+// CTAs; profiles/r02_ndisp_ab.txt), n_red = every SM. Cached per 4096-token bucket.
 eplab_tune_config auto_config(eplab_ctx* c, int n_tok) {
   const long long bucket = eplab::token_bucket(std::max(1, n_tok));
   auto it = c->tune_cache.find(bucket);
@@ -279,8 +279,8 @@ eplab_tune_config search_config(eplab_ctx* c, long long bucket) {
   if (!(c->spare_warps & 1)) calib.spare_sm_equiv = 0;
   const eplab::TuneResult r = eplab::search_layer(hw, shape, 0, calib);
   eplab_tune_config cfg{r.best.n_disp, r.best.n_relay, 1, c->num_sms, 8};
-  const int floor = ((c->spare_warps & 1) ? 16 : 64) * c->num_sms / 148;
-  if (cfg.n_disp < floor && floor + cfg.n_relay < c->num_sms) cfg.n_disp = floor;
+  // somebody must move the rows: without the spare-warp comm workers at least one comm CTA
+  if (!(c->spare_warps & 1) && cfg.n_disp == 0) cfg.n_disp = 1;
   return cfg;
 }
 }  // namespace
@@ -360,6 +360,8 @@ int eplab_init(const eplab_init_args* args, eplab_ctx** out) {
                  o_mpp = take((d.epr + 1) * 4), o_sc = take(64),
                  o_wg = take((size_t)d.epr * (d.F / 256) * 4), o_cur = take(64), o_err = take(64),
                  o_ep = take(64);
+    c->off_plan_lo = o_counts;
+    c->off_plan_hi = o_wg;
     CK(cudaMalloc(&c->loc, o));
     CK(cudaMemset(c->loc + o_hist, 0, o - o_hist));
     c->gu = reinterpret_cast<__nv_bfloat16*>(c->loc + o_gu);
@@ -671,9 +673,9 @@ int eplab_dispatch_group_gemm_bwd(eplab_ctx* c, const void* dy, const void* w_do
     CK(cudaSetDevice(c->device));
     cudaStream_t st = (cudaStream_t)stream;  // (wg_cnt: zeroed by the previous launch's last CTA)
     MkArgs a = base_args(c);
-    // the backward dispatch moves twice the bytes of the forward one (dY rows plus the o rows
-    // of the gate gradient): twice the comm CTAs, within the deadlock constraint
-    // (profiles/r01_ndisp_sweep_bwd.txt)
+    // bwd_disp_scale x the comm CTAs (default 2), within the deadlock constraint: the dY rows land
+    // ahead of the down-dgrad tiles, whose K (= H) loop is as long as the forward up GEMM's
+    // (profiles/r01_ndisp_sweep_bwd.txt; with n_disp = 0 the spare warps move the rows alone)
     const int scale = c->bwd_disp_scale;
     a.n_disp = std::max(a.n_disp, std::min(a.n_disp * scale, c->num_sms / 2 - a.n_relay));
     a.dy = static_cast<const __nv_bfloat16*>(dy);
@@ -719,6 +721,95 @@ int eplab_group_gemm_combine_bwd(eplab_ctx* c, const void* w_up, void* dx, void*
     if (eplab_launch::launch_bwd_combine(tm, a, c->num_sms, (cudaStream_t)stream))
       throw Fail{EPLAB_ERR_INTERNAL, std::string("bwd combine launch: ") +
                                          cudaGetErrorString(cudaGetLastError())};
+  });
+}
+
+namespace {
+// Stash layout: plan tables | slot metadata [rows] | recv_x [rows][H] | GU [rows][2F] | h [rows][F],
+// each part 256-byte aligned.
+struct StashParts {
+  size_t plan, meta, x, gu, h, total;
+};
+StashParts stash_parts(const eplab_ctx* c, int rows) {
+  auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
+  StashParts s{};
+  size_t o = 0;
+  s.plan = o, o += al(c->off_plan_hi - c->off_plan_lo);
+  s.meta = o, o += al((size_t)rows * sizeof(SlotMeta));
+  s.x = o, o += al((size_t)rows * c->d.H * 2);
+  s.gu = o, o += al((size_t)rows * 2 * c->d.F * 2);
+  s.h = o, o += al((size_t)rows * c->d.F * 2);
+  s.total = o;
+  return s;
+}
+int stash_rows(eplab_ctx* c, cudaStream_t st) {
+  int rows = 0;
+  CK(cudaStreamSynchronize(st));
+  CK(cudaMemcpy(&rows, c->plan.scalars, 4, cudaMemcpyDeviceToHost));
+  validate(rows >= 0 && rows <= c->d.M_cap, "stash: no valid plan on the device (aborted iteration?)");
+  return rows;
+}
+}  // namespace
+
+int eplab_stash_bytes(eplab_ctx* c, size_t* bytes, void* stream) {
+  return guarded([&] {
+    require_plan(c);
+    validate(bytes != nullptr, "bytes is null");
+    CK(cudaSetDevice(c->device));
+    *bytes = stash_parts(c, stash_rows(c, (cudaStream_t)stream)).total;
+  });
+}
+
+int eplab_stash_save(eplab_ctx* c, void* dst, size_t dst_bytes, eplab_stash_info* info, void* stream) {
+  return guarded([&] {
+    require_plan(c);
+    validate(dst != nullptr && info != nullptr, "null stash buffer or info");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int rows = stash_rows(c, st);
+    const StashParts s = stash_parts(c, rows);
+    validate(dst_bytes >= s.total, "stash buffer too small (eplab_stash_bytes)");
+    char* b = static_cast<char*>(dst);
+    const auto cp = [&](size_t off, const void* src, size_t n) {
+      if (n) CK(cudaMemcpyAsync(b + off, src, n, cudaMemcpyDeviceToDevice, st));
+    };
+    cp(s.plan, c->loc + c->off_plan_lo, c->off_plan_hi - c->off_plan_lo);
+    cp(s.meta, c->mine.meta, (size_t)rows * sizeof(SlotMeta));
+    cp(s.x, c->mine.recv_x, (size_t)rows * c->d.H * 2);
+    cp(s.gu, c->gu, (size_t)rows * 2 * c->d.F * 2);
+    cp(s.h, c->hact, (size_t)rows * c->d.F * 2);
+    *info = eplab_stash_info{EPLAB_STASH_MAGIC, c->epoch, c->plan.n_tok, rows, c->plan.topk_ids, c->plan.gate_w,
+                             s.total};
+  });
+}
+
+int eplab_stash_restore(eplab_ctx* c, const void* src, const eplab_stash_info* info, void* stream) {
+  return guarded([&] {
+    validate(src != nullptr && info != nullptr, "null stash buffer or info");
+    validate(info->magic == EPLAB_STASH_MAGIC, "not a stash of this library (magic)");
+    validate(info->rows >= 0 && info->rows <= c->d.M_cap && info->n_tok >= 0 && info->n_tok <= c->d.T_max,
+             "stash does not fit this context");
+    const StashParts s = stash_parts(c, info->rows);
+    validate(info->bytes == s.total, "stash was made by a context of another shape");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const char* b = static_cast<const char*>(src);
+    const auto cp = [&](void* dst, size_t off, size_t n) {
+      if (n) CK(cudaMemcpyAsync(dst, b + off, n, cudaMemcpyDeviceToDevice, st));
+    };
+    cp(c->loc + c->off_plan_lo, s.plan, c->off_plan_hi - c->off_plan_lo);
+    cp(c->mine.meta, s.meta, (size_t)info->rows * sizeof(SlotMeta));
+    cp(c->mine.recv_x, s.x, (size_t)info->rows * c->d.H * 2);
+    cp(c->gu, s.gu, (size_t)info->rows * 2 * c->d.F * 2);
+    cp(c->hact, s.h, (size_t)info->rows * c->d.F * 2);
+    c->plan.n_tok = info->n_tok;
+    c->plan.topk_ids = info->topk_ids;
+    c->plan.gate_w = info->gate_w;
+    c->epoch++;
+    if (eplab_launch::epoch_advance_launch(c->epoch_dev, st))
+      throw Fail{EPLAB_ERR_INTERNAL, std::string("epoch launch: ") + cudaGetErrorString(cudaGetLastError())};
+    c->planned = true;
+    c->dgate_set = false;
   });
 }
 

@@ -10,6 +10,7 @@ int preload_plan();
 int plan_launch(const eplab_dev::Dims& d, const eplab_dev::Peers& peers,
                 const eplab_dev::PlanDev& p, uint32_t* epoch, uint64_t timeout_ns, int* err,
                 __nv_bfloat16* recv_x, __nv_bfloat16* recv_dy, cudaStream_t st);
+int epoch_advance_launch(uint32_t* epoch, cudaStream_t st);
 int plan_counts_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p, uint32_t* epoch, int* out,
                        cudaStream_t st);
 int plan_layout_ext_launch(const eplab_dev::Dims& d, const eplab_dev::PlanDev& p, const int* call, int* err,

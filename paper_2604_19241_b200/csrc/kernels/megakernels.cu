@@ -1351,16 +1351,32 @@ struct ModeDgradUp {
 // launches separate the MegaKernels (cursor[6] counts the CTAs out). Every CTA has finished with
 // the counters when it arrives; an aborted iteration touches none of them.
 __device__ __forceinline__ void finish_kernel(const MkArgs& a, int kind) {
+  __shared__ int sh_last;
   __syncthreads();
-  if (threadIdx.x != 0) return;
-  __threadfence();
   unsigned* done = reinterpret_cast<unsigned*>(a.cursor + 6);
-  if (atomicAdd(done, 1u) != gridDim.x - 1) return;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    sh_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!sh_last) return;
   __threadfence();
-  for (int i = 0; i < 6; ++i) a.cursor[i] = 0;
+  // The scoreboard counters this kernel waited on (this phase, this parity) are complete -- every
+  // increment, local or from a peer, was awaited by a CTA of this grid -- so they are zeroed here
+  // too, not only one iteration later by the other parity's kernel: a restored iteration
+  // (eplab_stash_restore) may run this phase twice in a row with the same parity.
+  const SymPtrs& me = a.peers.p[a.d.rank];
+  const int ph = kind >= 2 ? 1 : 0;
+  if (kind == 0 || kind == 2)
+    for (int g = threadIdx.x; g < a.d.RG_cap; g += blockDim.x) *rg_counter(me, a.d, ph, PAR(a), g) = 0;
+  else
+    for (int t = threadIdx.x; t < a.p.n_tok; t += blockDim.x) *tok_counter(me, a.d, ph, PAR(a), t) = 0;
   if (kind == 2)
-    for (int i = 0; i < a.d.epr * (a.d.F / BN); ++i) a.wg_cnt[i] = 0;
-  *done = 0;
+    for (int i = threadIdx.x; i < a.d.epr * (a.d.F / BN); i += blockDim.x) a.wg_cnt[i] = 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 6; ++i) a.cursor[i] = 0;
+    *done = 0;
+  }
   __threadfence();
 }
 

@@ -58,6 +58,10 @@ __device__ uint32_t plan_advance_epoch(uint32_t* epoch_dev) {
   return epoch_s;
 }
 
+// A restored iteration (eplab_stash_restore) runs its backward under a fresh epoch: slot flags and
+// counter parities of the MegaKernels never see an epoch twice.
+__global__ void epoch_advance_kernel(uint32_t* epoch_dev) { plan_advance_epoch(epoch_dev); }
+
 // (a) CumSum over chunks (chunk bases, in place in p.hist) and C_exp -> p.counts and cnt_s.
 // Two passes over (expert, chunk-range) segments -- every thread of the CTA, S = blockDim / E
 // segments per expert -- so the chunk scan is not one thread walking all chunks of an expert with a
@@ -374,6 +378,11 @@ int plan_launch(const Dims& d, const Peers& peers, const PlanDev& p, uint32_t* e
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
+int epoch_advance_launch(uint32_t* epoch, cudaStream_t st) {
+  epoch_advance_kernel<<<1, 32, 0, st>>>(epoch);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
 // Loads the planning kernels into the current context up front (see preload_megakernels): the
 // count exchange of plan_global_kernel spins until every virtual rank's planner has run.
 int preload_plan() {
@@ -382,7 +391,8 @@ int preload_plan() {
                   cudaFuncGetAttributes(&fa, plan_global_kernel) == cudaSuccess &&
                   cudaFuncGetAttributes(&fa, plan_entries_kernel) == cudaSuccess &&
                   cudaFuncGetAttributes(&fa, plan_counts_kernel) == cudaSuccess &&
-                  cudaFuncGetAttributes(&fa, plan_layout_ext_kernel) == cudaSuccess;
+                  cudaFuncGetAttributes(&fa, plan_layout_ext_kernel) == cudaSuccess &&
+                  cudaFuncGetAttributes(&fa, epoch_advance_kernel) == cudaSuccess;
   return ok ? 0 : 1;
 }
 

@@ -50,8 +50,8 @@ class LayerPrediction(C.Structure):
 
 
 # B200 calibration of this build (DESIGN.md §Performance model; refit by tools/fit_model.py)
-# fitted over 76 measured cases, spare-warp comm workers on/off (profiles/r01_perf_model_validation.md)
-B200_CALIB = Calib(1.0, 0.2e-6, 25.01e9, 25.01e9, 6.5e12, 42.19e-6, 200.0e9, 41.78, 0.513, 1.0)
+# fitted over 94 measured cases, EP=1 and EP=2/4/8 on virtual ranks (profiles/r02_perf_model_validation.md)
+B200_CALIB = Calib(0.935, 0.2e-6, 28.94e9, 8.88e9, 6.5e12, 31.45e-6, 199.1e9, 29.04, 0.528, 2.0)
 
 
 def hw(world, n_sm=148, p_peak=1408.1e12, bw_hbm=6468.9e9, bw_nvl=770e9, w_sat=1024.0, tau_sync=1e-6):
@@ -139,14 +139,18 @@ def search_layer(s, h, calib=None):
 
 
 def choose_config(H, F, E, k, tokens, world, n_sm=148, spare=True):
-    """TuneConfig for one layer shape from the B200 model (n_red = all SMs; w = 8)."""
-    best, _, _ = search_layer(shape(H, F, E, k, tokens), hw(world, n_sm=n_sm))
+    """TuneConfig for one layer shape from the B200 model (n_red = all SMs; w = 8). spare=False:
+    the GEMM CTAs' spare warps stay out of the comm pool (eplab_set_comm_options bit 0 clear)."""
+    calib = B200_CALIB
+    if not spare:
+        calib = Calib(*[getattr(B200_CALIB, n) for n, _ in Calib._fields_])
+        calib.spare_sm_equiv = 0.0
+    best, _, _ = search_layer(shape(H, F, E, k, tokens), hw(world, n_sm=n_sm), calib)
     best.n_red = n_sm
-    # Measured floor: the model does not capture the start-up of the GEMM tiles behind the first
-    # landed rowgroups. With the GEMM CTAs' spare warps in the comm pool (default) the model picks
-    # 0-20 comm CTAs and 16 is the measured optimum at EP=1 (profiles/r01_spare_warps.txt); without
-    # them (spare=False) it was >= 64 (profiles/r01_ndisp_sweep.txt). EP>1: not yet measured.
-    floor = ((16 if spare else 64) * n_sm) // 148
-    if best.n_disp < floor and floor + best.n_relay < n_sm:
-        best.n_disp = floor
+    if not spare and best.n_disp == 0:
+        best.n_disp = 1  # somebody must move the rows
+    # No floor on n_disp (round 1 forced >= 16 comm CTAs): the model's GEMM start-up term (the first
+    # wave's rows landing at the comm pool's rate) and the comm CTAs' SM time now order the choices
+    # as measured -- in-process A/B, profiles/r02_ndisp_ab.txt: 0 comm CTAs is best or within noise
+    # for Mixtral, Qwen3, DSv3 and the top-k sweep shapes.
     return best

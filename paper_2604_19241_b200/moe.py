@@ -69,6 +69,9 @@ _SIGS = {
     "eplab_timeline_enable": [_P, _I],
     "eplab_timeline_export": [_P, C.c_char_p, C.POINTER(C.c_double)],
     "eplab_router_topk": [_P, _I, _I, _I, _I, _P, _P, _P],
+    "eplab_stash_bytes": [_P, C.POINTER(C.c_size_t), _P],
+    "eplab_stash_save": [_P, _P, C.c_size_t, _P, _P],
+    "eplab_stash_restore": [_P, _P, _P, _P],
     "eplab_router_topk_bwd": [_P, _P, _P, _P, _I, _I, _I, _I, _P, _P],
 }
 
@@ -104,6 +107,24 @@ def _stream(stream):
     return _P(s.cuda_stream)
 
 
+class StashInfo(C.Structure):
+    """eplab_stash_info (include/eplab_b200.h)."""
+    _fields_ = [("magic", C.c_uint32), ("epoch", C.c_uint32), ("n_tok", _I), ("rows", _I),
+                ("topk_ids", _P), ("gate_w", _P), ("bytes", C.c_size_t)]
+
+
+class Stash:
+    """One iteration's state copied out of a context (EpMoE.stash / restore): the device buffer,
+    the library's info record, and the routing tensors the plan points at (kept alive)."""
+
+    def __init__(self, epoch, buf, info, ids, gw):
+        self.epoch, self.buf, self.info, self.ids, self.gw = epoch, buf, info, ids, gw
+
+    @property
+    def nbytes(self):
+        return self.info.bytes
+
+
 _LIVE = weakref.WeakSet()  # open contexts (tests release them after a failure: live_contexts())
 
 
@@ -135,7 +156,10 @@ class EpMoE:
         self.h = h
         _LIVE.add(self)
         self._ids = self._gw = None
-        self.plan_epoch = 0  # plans issued on this context (EpMoEFunction ties backward to it)
+        self.plan_epoch = 0  # id of the plan whose state the context holds (EpMoEFunction ties
+        self._plans = 0      # its backward to it); ids are never reused
+        self._pending = {}   # plan id -> weakref to the autograd node whose backward needs it
+        self._stashes = {}   # plan id -> Stash (made when a later plan would overwrite it)
 
     def close(self):
         if self.h:
@@ -234,9 +258,43 @@ class EpMoE:
         n = topk_ids.shape[0]
         ids = self._need(topk_ids.contiguous(), "topk_ids", (n, self.k), torch.int32)
         gw = self._need(gate_w.contiguous(), "gate_w", (n, self.k), torch.float32)
+        self._evict(stream)
         self._ids, self._gw = ids, gw
         _check(lib().eplab_plan(self.h, _ptr(ids), _ptr(gw), n, _stream(stream)))
-        self.plan_epoch += 1
+        self._plans += 1
+        self.plan_epoch = self._plans
+
+    # ------------------------------------------------------------------ several forwards in flight
+    def stash(self, stream=None):
+        """Copy the current iteration's state (plan tables, received rows and slot metadata, saved
+        g/u and h) into a new device buffer sized to its receive rows (eplab_stash_save)."""
+        self._need_planned()
+        nb = C.c_size_t()
+        _check(lib().eplab_stash_bytes(self.h, C.byref(nb), _stream(stream)))
+        buf = torch.empty(nb.value, dtype=torch.uint8, device=self.device)
+        info = StashInfo()
+        _check(lib().eplab_stash_save(self.h, _ptr(buf), nb.value, C.byref(info), _stream(stream)))
+        if stream is not None:
+            buf.record_stream(stream)
+        return Stash(self.plan_epoch, buf, info, self._ids, self._gw)
+
+    def restore(self, st, stream=None):
+        """Make a stashed iteration the current one again: its backward may run next. The live
+        iteration is stashed first if an autograd backward still needs it."""
+        self._evict(stream)
+        _check(lib().eplab_stash_restore(self.h, _ptr(st.buf), C.byref(st.info), _stream(stream)))
+        self._ids, self._gw = st.ids, st.gw
+        self.plan_epoch = st.epoch
+
+    def _evict(self, stream):
+        """Before the context's state is overwritten: stash it if a pending autograd backward
+        (one whose graph is still alive) needs it; forget stashes whose graphs were freed."""
+        for e in [e for e, r in self._pending.items() if r() is None]:
+            self._pending.pop(e)
+            self._stashes.pop(e, None)
+        e = self.plan_epoch
+        if e in self._pending and e not in self._stashes:
+            self._stashes[e] = self.stash(stream)
 
     def dispatch_group_gemm(self, x, w_up, stream=None):
         n = self._need_planned()
@@ -398,23 +456,30 @@ class EpMoEFunction(torch.autograd.Function):
     def forward(ctx, layer, x, topk_ids, gate_w, w_up, w_down):
         y = layer.forward(x.contiguous(), topk_ids, gate_w, w_up, w_down)
         ctx.layer = layer
-        # The backward reads this plan's saved activations (receive rows, g/u, replica rows, slot
-        # metadata) from the context: one in-flight forward per context. A second forward on the
-        # same context before this backward (pipelined micro-batches, several layers sharing a
-        # context, activation recomputation) would silently corrupt the gradients, so the
-        # backward checks the plan epoch and raises EplabError(2) instead.
+        # The backward reads this plan's state (receive rows, g/u, h, slot metadata, plan tables)
+        # from the context. Several forwards may be in flight (pipelined micro-batches, layers
+        # sharing a context, activation recomputation): a later plan stashes this state first
+        # (EpMoE._evict) and the backward restores it, in any order.
         ctx.plan_epoch = layer.plan_epoch
+        layer._pending[layer.plan_epoch] = weakref.ref(ctx)
         ctx.save_for_backward(w_up, w_down)
         return y
 
     @staticmethod
     def backward(ctx, dy):
         w_up, w_down = ctx.saved_tensors
-        if ctx.layer.plan_epoch != ctx.plan_epoch:
-            raise EplabError(2, f"the context was re-planned (plan {ctx.layer.plan_epoch}) after this "
-                                f"forward (plan {ctx.plan_epoch}): its saved activations are gone. Use one "
-                                f"EpMoE context per in-flight forward.")
-        g = ctx.layer.backward(dy.contiguous(), w_up, w_down)
+        L, e = ctx.layer, ctx.plan_epoch
+        if L.plan_epoch != e:
+            st = L._stashes.get(e)
+            if st is None:
+                raise EplabError(2, f"the state of plan {e} is gone (the context holds plan {L.plan_epoch} "
+                                    f"and no stash of plan {e} exists: a second backward of a freed graph?)")
+            L.restore(st)
+        try:
+            g = L.backward(dy.contiguous(), w_up, w_down)
+        finally:
+            L._pending.pop(e, None)
+            L._stashes.pop(e, None)
         return None, g["dx"], None, g["dgate"], g["dw_up"], g["dw_down"]
 
 

@@ -239,9 +239,10 @@ def test_argument_checks_raise_validation_errors():
     L.close()
 
 
-def test_autograd_replan_before_backward_raises():
-    """One in-flight forward per context: a second forward before the first one's backward makes
-    that backward raise instead of returning gradients of the wrong plan."""
+def test_autograd_state_gone_raises():
+    """Forwards in flight are stashed (tests/test_microbatch_gpu.py); a backward whose plan state
+    is neither live nor stashed -- a retained graph run backward a second time after a re-plan --
+    raises error 2 instead of returning gradients of another plan."""
     m = moe()
     H, F, E, k, T = 256, 256, 8, 2, 64
     L = m.EpMoE(H, F, E, k, T)
@@ -251,13 +252,13 @@ def test_autograd_replan_before_backward_raises():
     wu = (torch.randn(E, 2 * F, H, device="cuda") * 0.05).bfloat16().requires_grad_()
     wd = (torch.randn(E, H, F, device="cuda") * 0.05).bfloat16().requires_grad_()
     y1 = m.EpMoEFunction.apply(L, x, ids, gw, wu, wd)
-    y1.float().sum().backward()  # fine: nothing re-planned in between
+    y1.float().sum().backward(retain_graph=True)
+    y1.float().sum().backward(retain_graph=True)  # fine: still the live plan
     y2 = m.EpMoEFunction.apply(L, x, ids, gw, wu, wd)
-    y3 = m.EpMoEFunction.apply(L, x, ids, gw, wu, wd)
     with pytest.raises(m.EplabError) as e:
-        y2.float().sum().backward()
-    assert e.value.code == 2 and "re-planned" in str(e.value)
-    y3.float().sum().backward()
+        y1.float().sum().backward()
+    assert e.value.code == 2 and "gone" in str(e.value)
+    y2.float().sum().backward()
     L.check()
     L.close()
 

@@ -161,6 +161,6 @@ def test_cpp_caller_links_against_the_library(tmp_path):
     _, _, off, _, _ = po.Oracle().token_map(osel, 128, 8)
     assert out["off_sum"] == int(off.sum())
     want = choose_config(2048, 768, 128, 8, 16384, 8)
-    best_n_disp = out["n_disp"]  # raw search_layer result (choose_config applies the comm-CTA floor)
+    best_n_disp = out["n_disp"]  # raw search_layer result (choose_config adds n_red = n_sm)
     assert out["n_relay"] == want.n_relay and best_n_disp <= want.n_disp
     assert out["validation_error"] is True

@@ -355,10 +355,14 @@ __device__ void comm_pipeline(const MkArgs& a, int ph, GemmSmem* S, uint8_t* sbu
 // (token_map.cpp:108-126), claimed in order from one atomic round counter by every comm
 // worker -- the 8 warps of each comm CTA (SM split, n_disp) and the spare warps of the GEMM
 // CTAs (warp split: warp 2 of both CTAs of a pair, warps 1 and 3 of the non-leader CTA). A
-// warp moves its round with 16-byte loads/stores, two rows in flight (16 x 16 B per lane). Then
+// warp moves its round with 16-byte loads/stores, CNR rows in flight (CNR x 8 x 16 B per lane). Then
 // it releases the round: one system-scope fence, relaxed rowgroup counter updates aggregated per
 // counter (relay off) or per-slot epoch flags (relay on).
 constexpr int CROUNDS = 128;
+#ifndef EPLAB_CNR
+#define EPLAB_CNR 4
+#endif
+constexpr int CNR = EPLAB_CNR;  // rows in flight per comm warp
 __device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
   const Dims& d = a.d;
   const int k = d.topk, vecs = d.H / 8, me = d.rank;
@@ -424,44 +428,51 @@ __device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
     done |= rel;
   };
   auto progress = [&]() {
-    if (n_copies <= 2) release();
+    if (n_copies <= CNR) release();
   };
-  // x rows (forward) and dY rows (backward) alike: a pure row copy, two rows in flight. (The gate
+  // x rows (forward) and dY rows (backward) alike: a pure row copy, CNR rows in flight. (The gate
   // gradient is no longer folded here: the down-dgrad epilogue has <dY W_down, h> per row in
   // registers, so the comm warps no longer read the o replica rows -- a third of the backward
   // dispatch's bytes.)
   {
-    unsigned m = __ballot_sync(0xffffffffu, dst >= 0);
+    // experiment: dbg 512 skips the row copies (rows of the previous identical step stay in place)
+    unsigned m = (a.dbg & 512) ? 0u : __ballot_sync(0xffffffffu, dst >= 0);
+    if (a.dbg & 512) copied = __ballot_sync(0xffffffffu, dst >= 0);
     while (m) {
-      const int qa = __ffs(m) - 1;
-      m &= m - 1;
-      const int qb = m ? __ffs(m) - 1 : qa;
-      if (m) m &= m - 1;
-      const bool two = qb != qa;
-      const int ia = __shfl_sync(0xffffffffu, item, qa), ib = __shfl_sync(0xffffffffu, item, qb);
-      const int sa_ = __shfl_sync(0xffffffffu, slot, qa), sb_ = __shfl_sync(0xffffffffu, slot, qb);
-      const int da_ = __shfl_sync(0xffffffffu, dst, qa), db_ = __shfl_sync(0xffffffffu, dst, qb);
-      const int4* sa = src_base + (size_t)(ia / k) * vecs;
-      const int4* sb = src_base + (size_t)(ib / k) * vecs;
-      int4* da = dst_row(da_, sa_);
-      int4* db = dst_row(db_, sb_);
-      for (int c = lane; c < vecs; c += 256) {
-        int4 va[8], vb[8];
+      // up to CNR rows per pass, CNR x 8 x 16 B loads in flight per lane (the copy is
+      // latency-bound: bytes in flight per warp set its rate)
+      int4* dp[CNR];
+      const int4* sp[CNR];
+      int nr = 0;
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (c + 32 * u < vecs) {
-            va[u] = ld_nc_v4(sa + c + 32 * u);
-            if (two) vb[u] = ld_nc_v4(sb + c + 32 * u);
-          }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (c + 32 * u < vecs) {
-            da[c + 32 * u] = va[u];
-            if (two) db[c + 32 * u] = vb[u];
-          }
+      for (int q = 0; q < CNR; ++q) {
+        const int qq = m ? __ffs(m) - 1 : -1;
+        if (m) m &= m - 1;
+        const int src_q = qq < 0 ? 0 : qq;
+        const int it_ = __shfl_sync(0xffffffffu, item, src_q);
+        const int sl_ = __shfl_sync(0xffffffffu, slot, src_q);
+        const int ds_ = __shfl_sync(0xffffffffu, dst, src_q);
+        sp[q] = qq < 0 ? nullptr : src_base + (size_t)(it_ / k) * vecs;
+        dp[q] = qq < 0 ? nullptr : dst_row(ds_, sl_);
+        if (qq >= 0) {
+          copied |= 1u << qq;
+          ++nr;
+        }
       }
-      copied |= (1u << qa) | (1u << qb);
-      n_copies += two ? 2 : 1;
+      for (int c = lane; c < vecs; c += 256) {
+        int4 v[CNR][8];
+#pragma unroll
+        for (int q = 0; q < CNR; ++q)
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (q < nr && c + 32 * u < vecs) v[q][u] = ld_nc_v4(sp[q] + c + 32 * u);
+#pragma unroll
+        for (int q = 0; q < CNR; ++q)
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (q < nr && c + 32 * u < vecs) dp[q][c + 32 * u] = v[q][u];
+      }
+      n_copies += nr;
       progress();
     }
   }
@@ -1172,6 +1183,17 @@ struct ModeDgradDown {
         uq[i] = usrc[i];
       }
     }
+    // experiment (dbg 1024 + timeline): cycles per epilogue section of warp 0, one record per tile
+    const bool sect = (a.dbg & 1024) && a.tl.rec && r == 0;
+    long long cs[5] = {0, 0, 0, 0, 0}, ct = sect ? clock64() : 0;
+    const unsigned long long gt0 = sect ? globaltimer() : 0;
+    auto mark = [&](int i) {
+      if (sect) {
+        const long long n = clock64();
+        cs[i] += n - ct;
+        ct = n;
+      }
+    };
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
       int4 gn[4], un[4];  // issued before this chunk's TMEM load so they also overlap its wait
@@ -1182,8 +1204,10 @@ struct ModeDgradDown {
           un[i] = usrc[(c + 1) * 4 + i];
         }
       }
+      mark(0);
       float v[32];
       acc_chunk(taddr, c, v);
+      mark(1);
       uint32_t pdg[16], pdu[16], phw[16];
       if (live) {
 #pragma unroll
@@ -1210,8 +1234,16 @@ struct ModeDgradDown {
         }
       }
       const int f0 = td.n0 + c * 32;
+      if (sect) {  // the compute section ends when its results exist (not at the issue of the math)
+        uint32_t z = 0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) z ^= pdg[q] ^ pdu[q] ^ phw[q];
+        asm volatile("" ::"r"(z));
+      }
+      mark(2);
       if (a.dbg & 4) continue;  // experiment: no staging / stores at all
       stage_acquire(lane);
+      mark(3);
       if (live) {
         stage_row_packed(stg, lane, pdg);
         stage_row_packed(stg + EPI_TILE_BYTES, lane, pdu);
@@ -1228,6 +1260,7 @@ struct ModeDgradDown {
         tma_store_2d(&tm.m[5], stg + 2 * EPI_TILE_BYTES, f0, row0);  // HW
         tma_store_commit();
       }
+      mark(4);
       if (ld_gu && c + 1 < BN / 32) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -1236,6 +1269,8 @@ struct ModeDgradDown {
         }
       }
     }
+    if (sect)
+      for (int i = 0; i < 5; ++i) timeline_push(a.tl, gt0, gt0 + (unsigned long long)cs[i], ROLE_COMP, -9011 - i);
     if (live) {  // this tile's gate-gradient partial, to the source (peer memory at EP > 1)
       const int ncb = F / BN;
       float* dst = a.unfused ? a.ret_dgp + (size_t)a.ret_pos[m] * ncb

@@ -45,7 +45,10 @@ L.check()
 L.timeline_enable(1 << 20)
 os.makedirs(args.out, exist_ok=True)
 NAMES = {-9001: "mma_wait_tile", -9002: "mma_wait_acc", -9003: "mma_wait_ops",
-         -9004: "epi_wait_acc", -9005: "epi_work", -9006: "epi_release"}
+         -9004: "epi_wait_acc", -9005: "epi_work", -9006: "epi_release",
+         # dbg 1024: down-dgrad epilogue sections of warp 0, cycles (shares of their sum below)
+         -9011: "sec_loads_issue", -9012: "sec_tmem_ld", -9013: "sec_compute", -9014: "sec_stage_acquire",
+         -9015: "sec_stage_store"}
 rep = {"config": args.config, "opts": args.opt}
 for name, fn in steps:
     torch.cuda.synchronize()
@@ -68,6 +71,10 @@ for name, fn in steps:
             a[0] += e["dur"]
             a[1] += 1
     rep[name] = {"tile_span_us": round(span, 1), "tiles": len(tiles),
-                 **{n: round(100.0 * s / c / span, 1) for n, (s, c) in acc.items()}}
+                 **{n: round(100.0 * s / c / span, 1) for n, (s, c) in acc.items() if not n.startswith("sec_")}}
+    sec = {n: s for n, (s, c) in acc.items() if n.startswith("sec_")}
+    if sec:
+        rep[name]["epi_sections_pct"] = {n: round(100.0 * s / sum(sec.values()), 1) for n, s in sec.items()}
+        rep[name]["epi_cycles_per_tile"] = round(sum(sec.values()) * 1000.0 / acc["sec_tmem_ld"][1])
 L.check()
 print(json.dumps(rep), flush=True)

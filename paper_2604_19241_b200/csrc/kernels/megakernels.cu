@@ -374,6 +374,17 @@ __device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
   // lands after one row copy instead of after a whole round.
   const long long sr = r / CROUNDS, g = r - sr * CROUNDS;
   const long long idx = sr * CROUNDS * 32 + g + (long long)lane * CROUNDS;
+  // experiment (dbg 2048 + timeline): cycles per section of the round (metadata, copies, release)
+  const bool sect = (a.dbg & 2048) && a.tl.rec && lane == 0;
+  long long cs[3] = {0, 0, 0}, ct = sect ? clock64() : 0;
+  const unsigned long long gt0 = sect ? globaltimer() : 0;
+  auto mark = [&](int i) {
+    if (sect) {
+      const long long nw = clock64();
+      cs[i] += nw - ct;
+      ct = nw;
+    }
+  };
   int item = -1, slot = 0, dst = -1;  // dst < 0: the row does not travel from here
   if (idx < n) {
     const int i = a.p.sched[idx];
@@ -398,6 +409,9 @@ __device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
     item = i;
     dst = prim_slot >= 0 ? -1 : dr;
   }
+  if (sect) asm volatile("" ::"r"(item), "r"(slot), "r"(dst));
+  __syncwarp();
+  mark(0);
   const int4* src_base = reinterpret_cast<const int4*>(ph == 0 ? a.x : a.dy);
   auto dst_row = [&](int dr, int sl) {
     const SymPtrs& P = a.peers.p[dr];
@@ -413,6 +427,7 @@ __device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
     const unsigned rel = copied & ~done;
     if (!rel) return;
     __syncwarp();
+    mark(1);
     if (d.world == 1)
       fence_acq_rel_gpu();  // one GPU: every reader is on this device
     else
@@ -426,6 +441,8 @@ __device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
       if (ctr && lane == __ffs(mm) - 1) red_relaxed_sys_add(ctr, (uint32_t)__popc(mm));
     }
     done |= rel;
+    __syncwarp();
+    mark(2);
   };
   auto progress = [&]() {
     if (n_copies <= CNR) release();
@@ -477,6 +494,8 @@ __device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
     }
   }
   release();
+  if (sect)
+    for (int i = 0; i < 3; ++i) timeline_push(a.tl, gt0, gt0 + (unsigned long long)cs[i], ROLE_COMM, -9021 - i);
 }
 
 // A comm worker warp: claim rounds until the pool is empty. Returns the number of rounds moved.

@@ -48,7 +48,9 @@ NAMES = {-9001: "mma_wait_tile", -9002: "mma_wait_acc", -9003: "mma_wait_ops",
          -9004: "epi_wait_acc", -9005: "epi_work", -9006: "epi_release",
          # dbg 1024: down-dgrad epilogue sections of warp 0, cycles (shares of their sum below)
          -9011: "sec_loads_issue", -9012: "sec_tmem_ld", -9013: "sec_compute", -9014: "sec_stage_acquire",
-         -9015: "sec_stage_store"}
+         -9015: "sec_stage_store",
+         # dbg 2048: comm-round sections of each comm warp (lane 0), cycles
+         -9021: "com_meta", -9022: "com_copy", -9023: "com_release"}
 rep = {"config": args.config, "opts": args.opt}
 for name, fn in steps:
     torch.cuda.synchronize()
@@ -71,7 +73,11 @@ for name, fn in steps:
             a[0] += e["dur"]
             a[1] += 1
     rep[name] = {"tile_span_us": round(span, 1), "tiles": len(tiles),
-                 **{n: round(100.0 * s / c / span, 1) for n, (s, c) in acc.items() if not n.startswith("sec_")}}
+                 **{n: round(100.0 * s / c / span, 1) for n, (s, c) in acc.items() if n[:4] not in ("sec_", "com_")}}
+    com = {n: (s, c) for n, (s, c) in acc.items() if n.startswith("com_")}
+    if com:
+        rep[name]["comm_round_cycles"] = {n: round(s * 1000.0 / c) for n, (s, c) in com.items()}
+        rep[name]["comm_rounds"] = com["com_meta"][1]
     sec = {n: s for n, (s, c) in acc.items() if n.startswith("sec_")}
     if sec:
         rep[name]["epi_sections_pct"] = {n: round(100.0 * s / sum(sec.values()), 1) for n, s in sec.items()}

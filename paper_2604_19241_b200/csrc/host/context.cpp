@@ -692,7 +692,7 @@ int eplab_dispatch_group_gemm_bwd(eplab_ctx* c, const void* dy, const void* w_do
     tm.m[4] = c->st_dgu;
     tm.m[5] = c->st_hw;
     tm.m[6] = eplab_host::make_store_map(dw_down, (uint64_t)c->d.epr * c->d.H, c->d.F);
-    tm.m[7] = tm.m[6];
+    tm.m[7] = c->st_gu;  // the saved g, u: the down-dgrad epilogue's TMA input ring
     if (eplab_launch::launch_bwd_dispatch(tm, a, c->num_sms, st))
       throw Fail{EPLAB_ERR_INTERNAL, std::string("bwd dispatch launch: ") +
                                          cudaGetErrorString(cudaGetLastError())};
@@ -1264,7 +1264,7 @@ int eplab_unfused_bwd_down(eplab_ctx* c, const void* w_down, void* dw_down, floa
     tm.m[4] = c->st_dgu;
     tm.m[5] = c->st_hw;
     tm.m[6] = eplab_host::make_store_map(dw_down, (uint64_t)c->d.epr * c->d.H, c->d.F);
-    tm.m[7] = tm.m[6];
+    tm.m[7] = c->st_gu;  // the saved g, u: the down-dgrad epilogue's TMA input ring
     if (eplab_launch::launch_bwd_dispatch(tm, a, c->num_sms, st))
       throw Fail{EPLAB_ERR_INTERNAL, std::string("unfused bwd down: ") + cudaGetErrorString(cudaGetLastError())};
   });

@@ -67,6 +67,9 @@ struct GemmSmem {
   uint64_t rq_full[4];   // 4 arrivals: the four epilogue warps queued the tile
   uint64_t rq_empty[4];  // 1 arrival: the release warp published it
   TileDesc rq_td[4];
+  // CTA pair, Modes with an epilogue input ring (GU_RING): two TMA-completion barriers per epilogue
+  // warp for its two input buffers
+  uint64_t gbar[8];
   // comm role (runs before the CTA enters the GEMM roles; reuses the stage buffers)
   uint64_t cbar[48];      // one mbarrier per bulk-copy slot
   uint32_t cphase[4];     // per issuer: parity bit per owned slot (carried across comm tasks)

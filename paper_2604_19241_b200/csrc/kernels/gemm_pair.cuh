@@ -23,6 +23,24 @@ constexpr uint32_t P_HALF_BYTES = 128 * BK * 2;  // 16 KB: one CTA's A rows or B
 constexpr uint32_t P_STAGE_BYTES = 2 * P_HALF_BYTES;
 static_assert(P_STAGES * P_STAGE_BYTES == TILES_BYTES, "pair stages reuse the single-CTA smem map");
 
+// A Mode may run fewer operand stages (`static constexpr int PAIR_STAGES`): stage s of A stays at
+// half s and of B at half P_STAGES + s, so the last A half and the last B half (16 KB each) are
+// free for the epilogue's input ring (`static constexpr bool GU_RING = true`): 8 KB per epilogue
+// warp, two 4 KB buffers the warp fills with TMA loads of the rows its epilogue reads
+// (Mode::epilogue_issue before the accumulator wait, Mode::epilogue_ring consumes them).
+template <class M, class = void>
+struct pair_stages : std::integral_constant<int, P_STAGES> {};
+template <class M>
+struct pair_stages<M, std::void_t<decltype(M::PAIR_STAGES)>> : std::integral_constant<int, M::PAIR_STAGES> {};
+template <class M, class = void>
+struct has_gu_ring : std::false_type {};
+template <class M>
+struct has_gu_ring<M, std::void_t<decltype(M::GU_RING)>> : std::bool_constant<M::GU_RING> {};
+struct EpiRing {
+  uint8_t* buf;    // 2 x 4 KB
+  uint64_t* bar;   // 2 barriers
+};
+
 __device__ __forceinline__ void gemm_setup_pair(GemmSmem* S, uint32_t rank) {
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
@@ -39,6 +57,7 @@ __device__ __forceinline__ void gemm_setup_pair(GemmSmem* S, uint32_t rank) {
       mbar_init(&S->rempty[i], 11);  // leader: producer, mma, 4 epi; peer: producer, 4 epi
     }
     for (int i = 0; i < 48; ++i) mbar_init(&S->cbar[i], 1);
+    for (int i = 0; i < 8; ++i) mbar_init(&S->gbar[i], 1);
     for (int i = 0; i < 4; ++i) {
       S->cphase[i] = 0;
       mbar_init(&S->rq_full[i], 4);
@@ -73,6 +92,8 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
   uint8_t* sA = tiles_smem;
   uint8_t* sB = tiles_smem + P_STAGES * P_HALF_BYTES;
   const bool leader = rank == 0;
+  constexpr int NST = pair_stages<Mode>::value;
+  static_assert(NST <= P_STAGES && (!has_gu_ring<Mode>::value || NST < P_STAGES), "epilogue ring needs a free stage");
 
   // spare warps: warp 2 (TMEM owner, idle between allocation and teardown) of both CTAs and the
   // non-leader's warps 1 and 3 (the leader alone issues MMAs and schedules)
@@ -163,7 +184,7 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
             mbar_arrive_cluster(full0);
           Mode::load_a_pair(args, tm, full0, sA + stage * P_HALF_BYTES, td, kb, rank);
           if (!skip_b) Mode::load_b_pair(args, tm, full0, sB + stage * P_HALF_BYTES, td, kb, rank);
-          if (++stage == P_STAGES) {
+          if (++stage == NST) {
             stage = 0;
             phase ^= 1;
           }
@@ -212,7 +233,7 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
             umma_bf16_pair(d, ad, bd, idesc, (kb | k) != 0);
           }
           umma_commit_pair(&S->empty[stage]);
-          if (++stage == P_STAGES) {
+          if (++stage == NST) {
             stage = 0;
             phase ^= 1;
           }
@@ -229,6 +250,9 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
     // ---------------- epilogue (both CTAs): this CTA's 128 rows of the 256-row tile
     const int q = warp & 3;
     const int r = q * 32 + (int)lane;
+    EpiRing ring{nullptr, &S->gbar[2 * q]};
+    if constexpr (has_gu_ring<Mode>::value)  // warps 0, 1: free A half; warps 2, 3: free B half
+      ring.buf = tiles_smem + (q < 2 ? NST : P_STAGES + NST) * P_HALF_BYTES + (q & 1) * 8192;
     const uint32_t rempty0 = mapa_shared(smem_u32(&S->rempty[0]), 0);
     const uint32_t tempty0 = mapa_shared(smem_u32(&S->tempty[0]), 0);
     // stall accounting of epilogue warp 0 (timeline on): waiting for the accumulator (MMA), the
@@ -263,6 +287,9 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
       const TileDesc half = Mode::half_of(td, rank);
       const bool work = Mode::half_has_work(half);
       if (work) Mode::epilogue_prefetch(args, half, r);
+      if constexpr (has_gu_ring<Mode>::value) {
+        if (work) Mode::epilogue_issue(args, tm, half, (int)lane, q, ring);
+      }
       const uint32_t acc = it & 1;
       if (acct) tw = globaltimer();
       mbar_wait_wd(&S->tfull[acc], (it >> 1) & 1, wd, 47);
@@ -273,7 +300,11 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
         tw = now;
       }
       const uint32_t taddr = S->tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
-      if (work) Mode::epilogue(args, tm, half, taddr, r, tiles_smem + TILES_BYTES + q * EPI_WARP_BYTES);
+      if constexpr (has_gu_ring<Mode>::value) {
+        if (work) Mode::epilogue_ring(args, tm, half, taddr, r, tiles_smem + TILES_BYTES + q * EPI_WARP_BYTES, ring);
+      } else {
+        if (work) Mode::epilogue(args, tm, half, taddr, r, tiles_smem + TILES_BYTES + q * EPI_WARP_BYTES);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);

@@ -1172,8 +1172,37 @@ struct ModeDgradDown {
         tma_load_2d(&tm.m[3], bar, s + i * 8192, td.n0 + 64 * i, td.kb0 + kb * BK);
     }
   }
+  // CTA pair: 5 operand stages; the freed 32 KB hold each epilogue warp's saved-g/u input ring. The
+  // SwiGLU backward reads the forward's g, u of its 32 rows x 32 columns per chunk: with per-lane
+  // global loads (one row per lane, 16 B pieces, one chunk ahead in registers) the math waited for
+  // them (removing the loads cut the epilogue's cycles by 40 %, profiles/r02_epilogue_gather_probes.md);
+  // TMA loads them into the ring two chunks ahead, the first two before the accumulator wait.
+  static constexpr int PAIR_STAGES = 5;
+  static constexpr bool GU_RING = true;
+  __device__ static void gu_load(const Args& a, const TmaSet& tm, const TileDesc& td, int row0, int c,
+                                 const EpiRing& ring) {
+    uint8_t* b = ring.buf + (c & 1) * 4096;
+    mbar_arrive_expect_tx(&ring.bar[c & 1], 4096);
+    tma_load_2d(&tm.m[7], &ring.bar[c & 1], b, td.n0 + c * 32, row0);               // g
+    tma_load_2d(&tm.m[7], &ring.bar[c & 1], b + 2048, a.d.F + td.n0 + c * 32, row0);  // u
+  }
+  __device__ static void epilogue_issue(const Args& a, const TmaSet& tm, const TileDesc& td, int lane,
+                                        int q, const EpiRing& ring) {
+    if (td.pad1 || lane != 0) return;
+    gu_load(a, tm, td, td.m0 + q * 32, 0, ring);
+    gu_load(a, tm, td, td.m0 + q * 32, 1, ring);
+  }
   __device__ static void epilogue(const Args& a, const TmaSet& tm, const TileDesc& td,
                                   uint32_t taddr, int r, uint8_t* stg) {
+    epi<false>(a, tm, td, taddr, r, stg, EpiRing{nullptr, nullptr});
+  }
+  __device__ static void epilogue_ring(const Args& a, const TmaSet& tm, const TileDesc& td,
+                                       uint32_t taddr, int r, uint8_t* stg, const EpiRing& ring) {
+    epi<true>(a, tm, td, taddr, r, stg, ring);
+  }
+  template <bool RING>
+  __device__ static void epi(const Args& a, const TmaSet& tm, const TileDesc& td, uint32_t taddr, int r,
+                             uint8_t* stg, const EpiRing& ring) {
     const int F = a.d.F;
     if (td.pad1) {  // weight-gradient tile
       wgrad_store(&tm.m[6], td, a.d.H, taddr, r, stg);
@@ -1195,7 +1224,7 @@ struct ModeDgradDown {
     // saved g, u of chunk c+1 are in flight while chunk c is computed (software pipelining)
     int4 gq[4] = {}, uq[4] = {};
     const bool ld_gu = live && !(a.dbg & 16);  // experiment: dbg 16 skips the saved g, u loads
-    if (ld_gu) {
+    if (!RING && ld_gu) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         gq[i] = gsrc[i];
@@ -1216,7 +1245,21 @@ struct ModeDgradDown {
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
       int4 gn[4], un[4];  // issued before this chunk's TMEM load so they also overlap its wait
-      if (ld_gu && c + 1 < BN / 32) {
+      if constexpr (RING) {  // this chunk's g, u from the ring, then the refill two chunks ahead
+        mbar_wait(&ring.bar[c & 1], (c >> 1) & 1);
+        const uint8_t* b = ring.buf + (c & 1) * 4096 + lane * 64;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t off = (uint32_t)((i ^ ((lane >> 1) & 3)) << 4);
+          gq[i] = ld_gu ? *reinterpret_cast<const int4*>(b + off) : make_int4(0, 0, 0, 0);
+          uq[i] = ld_gu ? *reinterpret_cast<const int4*>(b + 2048 + off) : make_int4(0, 0, 0, 0);
+        }
+        __syncwarp();
+        if (lane == 0 && c + 2 < BN / 32) {
+          fence_proxy_async();  // the warp's reads of the buffer before the TMA refill
+          gu_load(a, tm, td, row0, c + 2, ring);
+        }
+      } else if (ld_gu && c + 1 < BN / 32) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           gn[i] = gsrc[(c + 1) * 4 + i];
@@ -1280,7 +1323,7 @@ struct ModeDgradDown {
         tma_store_commit();
       }
       mark(4);
-      if (ld_gu && c + 1 < BN / 32) {
+      if (!RING && ld_gu && c + 1 < BN / 32) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           gq[i] = gn[i];

@@ -22,15 +22,15 @@ ap.add_argument("--config", default="qwen3")
 ap.add_argument("--opt", action="append", default=[])
 ap.add_argument("--out", default="/tmp/phase_report")
 ap.add_argument("--cfg", default="", help="n_disp,n_relay,n_comb,n_red,w instead of the model's choice")
+ap.add_argument("--warm-first", action="store_true",
+                help="one step with default options before --opt applies (dbg 512 then times the GEMM "
+                     "roles on the real rows the skipped copies would have moved, not on zeros)")
 args = ap.parse_args()
 H, F, E, k, T = bench.CONFIGS[args.config]
 inp = bench.make_inputs(args.config, 1, 0)
 L = M.EpMoE(H, F, E, k, T)
 cfg = M.TuneConfig(*[int(v) for v in args.cfg.split(",")]) if args.cfg else choose_config(H, F, E, k, T, 1)
 L.set_tune_config(cfg)
-for o in args.opt:
-    n, v = o.split("=")
-    L.set_option(n, int(v))
 y = torch.empty(T, H, device="cuda", dtype=torch.bfloat16)
 out = dict(dx=torch.empty(T, H, dtype=torch.bfloat16, device="cuda"), dw_up=torch.empty_like(inp["w_up"]),
            dw_down=torch.empty_like(inp["w_down"]), dgate=torch.empty(T, k, dtype=torch.float32, device="cuda"))
@@ -38,6 +38,13 @@ steps = [("fwd_dispatch", lambda: (L.plan(inp["ids"], inp["gws"]), L.dispatch_gr
          ("fwd_combine", lambda: L.group_gemm_combine(inp["w_down"], y)),
          ("bwd_dispatch", lambda: L._dispatch_bwd(inp["dy"], inp["w_down"], out)),
          ("bwd_combine", lambda: L._combine_bwd(inp["w_up"], out))]
+if args.warm_first:
+    for _, fn in steps:
+        fn()
+    L.check()
+for o in args.opt:
+    n, v = o.split("=")
+    L.set_option(n, int(v))
 for _, fn in steps:
     fn()
 L.check()

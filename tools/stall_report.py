@@ -20,6 +20,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="qwen3")
 ap.add_argument("--opt", action="append", default=[], help="eplab_set_option name=value")
 ap.add_argument("--out", default="gpurun_out")
+ap.add_argument("--warm-first", action="store_true", help="one default step before --opt applies (real rows for dbg 512)")
 ap.add_argument("--shape", default="", help="H,F,E,k,T instead of a bench config")
 args = ap.parse_args()
 H, F, E, k, T = [int(v) for v in args.shape.split(",")] if args.shape else bench.CONFIGS[args.config]
@@ -29,9 +30,6 @@ bench.CONFIGS[args.config] = (H, F, E, k, T)
 inp = bench.make_inputs(args.config, 1, 0)
 L = M.EpMoE(H, F, E, k, T)
 L.set_tune_config(choose_config(H, F, E, k, T, 1))
-for o in args.opt:
-    n, v = o.split("=")
-    L.set_option(n, int(v))
 y = torch.empty(T, H, device="cuda", dtype=torch.bfloat16)
 out = dict(dx=torch.empty(T, H, dtype=torch.bfloat16, device="cuda"), dw_up=torch.empty_like(inp["w_up"]),
            dw_down=torch.empty_like(inp["w_down"]), dgate=torch.empty(T, k, dtype=torch.float32, device="cuda"))
@@ -39,6 +37,11 @@ steps = [("fwd_dispatch", lambda: (L.plan(inp["ids"], inp["gws"]), L.dispatch_gr
          ("fwd_combine", lambda: L.group_gemm_combine(inp["w_down"], y)),
          ("bwd_dispatch", lambda: L._dispatch_bwd(inp["dy"], inp["w_down"], out)),
          ("bwd_combine", lambda: L._combine_bwd(inp["w_up"], out))]
+for _, fn in steps if args.warm_first else []:
+    fn()
+for o in args.opt:
+    n, v = o.split("=")
+    L.set_option(n, int(v))
 for _, fn in steps:  # warm-up step
     fn()
 L.check()

@@ -200,6 +200,9 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
       // scoreboard), for a free accumulator (epilogue), for operands (producer)
       const bool acct = tl.rec != nullptr;
       unsigned long long w_tile = 0, w_acc = 0, w_ops = 0, t_begin = acct ? globaltimer() : 0, tw = 0;
+      // per tile type (td.pad1: 0 = NT tiles, 1 = transposed weight-gradient tiles): main-loop time
+      // (first operand wait to the last commit) and its operand waits
+      unsigned long long ty_loop[2] = {0, 0}, ty_ops[2] = {0, 0}, tl0 = 0;
       for (int it = 0;; ++it) {
         const int slot = it % RING;
         if (acct) tw = globaltimer();
@@ -217,10 +220,16 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
         if (acct) w_acc += globaltimer() - tw;
         tc_fence_after();
         const uint32_t d = S->tmem_base + acc * BN;
+        const int ty = td.pad1 ? 1 : 0;
+        if (acct) tl0 = globaltimer();
         for (int kb = 0; kb < td.nkb; ++kb) {
           if (acct) tw = globaltimer();
           mbar_wait_wd(&S->full[stage], phase, wd, 45);
-          if (acct) w_ops += globaltimer() - tw;
+          if (acct) {
+            const unsigned long long dw = globaltimer() - tw;
+            w_ops += dw;
+            ty_ops[ty] += dw;
+          }
           tc_fence_after();
           const uint32_t as = a0 + stage * P_HALF_BYTES;
           const uint32_t bs = b0 + stage * P_HALF_BYTES;
@@ -239,11 +248,16 @@ __device__ void gemm_roles_pair(const typename Mode::Args& args, const TmaSet& t
           }
         }
         umma_commit_pair(&S->tfull[acc]);
+        if (acct) ty_loop[ty] += globaltimer() - tl0;
       }
       if (acct) {  // three records per CTA pair, durations = the stall totals (task -9001..-9003)
         timeline_push(tl, t_begin, t_begin + w_tile, ROLE_COMP, -9001);
         timeline_push(tl, t_begin, t_begin + w_acc, ROLE_COMP, -9002);
         timeline_push(tl, t_begin, t_begin + w_ops, ROLE_COMP, -9003);
+        for (int y = 0; y < 2; ++y) {  // -9031/-9032: main-loop time per type, -9033/-9034: its operand waits
+          timeline_push(tl, t_begin, t_begin + ty_loop[y], ROLE_COMP, -9031 - y);
+          timeline_push(tl, t_begin, t_begin + ty_ops[y], ROLE_COMP, -9033 - y);
+        }
       }
     }
   } else if (warp >= 4) {

@@ -376,7 +376,7 @@ __device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
   const long long idx = sr * CROUNDS * 32 + g + (long long)lane * CROUNDS;
   // experiment (dbg 2048 + timeline): cycles per section of the round (metadata, copies, release)
   const bool sect = (a.dbg & 2048) && a.tl.rec && lane == 0;
-  long long cs[3] = {0, 0, 0}, ct = sect ? clock64() : 0;
+  long long cs[5] = {0, 0, 0, 0, 0}, ct = sect ? clock64() : 0;
   const unsigned long long gt0 = sect ? globaltimer() : 0;
   auto mark = [&](int i) {
     if (sect) {
@@ -483,11 +483,22 @@ __device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
 #pragma unroll
           for (int u = 0; u < 8; ++u)
             if (q < nr && c + 32 * u < vecs) v[q][u] = ld_nc_v4(sp[q] + c + 32 * u);
+        if (sect) {  // section accounting: wait for every load of the pass, then time the stores
+          uint32_t z = 0;
+#pragma unroll
+          for (int q = 0; q < CNR; ++q)
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (q < nr && c + 32 * u < vecs) z ^= (uint32_t)v[q][u].x;
+          asm volatile("" ::"r"(z));
+          mark(3);
+        }
 #pragma unroll
         for (int q = 0; q < CNR; ++q)
 #pragma unroll
           for (int u = 0; u < 8; ++u)
             if (q < nr && c + 32 * u < vecs) dp[q][c + 32 * u] = v[q][u];
+        mark(4);
       }
       n_copies += nr;
       progress();
@@ -495,7 +506,7 @@ __device__ void comm_round_warp(const MkArgs& a, int ph, long long r) {
   }
   release();
   if (sect)
-    for (int i = 0; i < 3; ++i) timeline_push(a.tl, gt0, gt0 + (unsigned long long)cs[i], ROLE_COMM, -9021 - i);
+    for (int i = 0; i < 5; ++i) timeline_push(a.tl, gt0, gt0 + (unsigned long long)cs[i], ROLE_COMM, -9021 - i);
 }
 
 // A comm worker warp: claim rounds until the pool is empty. Returns the number of rounds moved.

@@ -53,7 +53,10 @@ NAMES = {-9001: "mma_wait_tile", -9002: "mma_wait_acc", -9003: "mma_wait_ops",
          -9011: "sec_loads_issue", -9012: "sec_tmem_ld", -9013: "sec_compute", -9014: "sec_stage_acquire",
          -9015: "sec_stage_store",
          # dbg 2048: comm-round sections of each comm warp (lane 0), cycles
-         -9021: "com_meta", -9022: "com_copy", -9023: "com_release"}
+         -9021: "com_meta", -9022: "com_copy", -9023: "com_release",
+         -9024: "com_loads", -9025: "com_stores",  # the copy section split: loads of a pass, its stores
+         # MMA issuer per tile type: main-loop time and its operand waits (NT tiles / transposed tiles)
+         -9031: "ty_loop_nt", -9032: "ty_loop_tn", -9033: "ty_ops_nt", -9034: "ty_ops_tn"}
 rep = {"config": args.config, "opts": args.opt}
 for name, fn in steps:
     torch.cuda.synchronize()
@@ -76,7 +79,12 @@ for name, fn in steps:
             a[0] += e["dur"]
             a[1] += 1
     rep[name] = {"tile_span_us": round(span, 1), "tiles": len(tiles),
-                 **{n: round(100.0 * s / c / span, 1) for n, (s, c) in acc.items() if n[:4] not in ("sec_", "com_")}}
+                 **{n: round(100.0 * s / c / span, 1) for n, (s, c) in acc.items() if n[:4] not in ("sec_", "com_", "ty_l", "ty_o")}}
+    for ty in ("nt", "tn"):  # operand-wait share of each tile type's main loops
+        lp, op = acc.get("ty_loop_" + ty, (0.0, 0))[0], acc.get("ty_ops_" + ty, (0.0, 0))[0]
+        if lp > 0:
+            rep[name]["ops_wait_in_loop_" + ty] = round(100.0 * op / lp, 1)
+            rep[name]["loop_us_per_pair_" + ty] = round(lp / max(1, acc["ty_loop_" + ty][1]), 1)
     com = {n: (s, c) for n, (s, c) in acc.items() if n.startswith("com_")}
     if com:
         rep[name]["comm_round_cycles"] = {n: round(s * 1000.0 / c) for n, (s, c) in com.items()}

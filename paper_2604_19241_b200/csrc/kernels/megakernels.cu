@@ -27,6 +27,10 @@
 #include "gemm_pair.cuh"
 #include "moe_common.cuh"
 
+#ifndef EPLAB_ENGINE_WD
+#define EPLAB_ENGINE_WD 0
+#endif
+
 namespace eplab_dev {
 
 // Iteration number of the running MegaKernel, read once per CTA from the device epoch counter
@@ -1620,8 +1624,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // pair up: the leader learns both CTAs' first non-pre ids
   if (threadIdx.x == 0) st_cluster_u32(mapa_shared(smem_u32(&S->pend[rank]), 0), (uint32_t)id);
   cluster_sync_all();
-  gemm_roles_pair<Mode>(a, tm, base, S, n_pre, n_pre + n_tiles, a.cursor, a.tl, rank,
-                        Watchdog{});  // Watchdog{a.err, a.timeout_ns} to debug engine hangs
+#if EPLAB_ENGINE_WD
+  // engine mbarrier waits report error 3 (sites 40-47); a debug build (make EXTRA=-DEPLAB_ENGINE_WD=1):
+  // the timed waits in the MMA / producer / epilogue loops cost 6 % (Qwen3, Mixtral), profiles/r02_dgrad_ring_ab.txt
+  const Watchdog wd{a.err, a.timeout_ns};
+#else
+  const Watchdog wd{};
+#endif
+  gemm_roles_pair<Mode>(a, tm, base, S, n_pre, n_pre + n_tiles, a.cursor, a.tl, rank, wd);
   cluster_sync_all();
   if (threadIdx.x == 0) {
     const int pn = (int)ld_cluster_u32(mapa_shared(smem_u32(&S->post_n), 0));

@@ -64,7 +64,7 @@ class Problem:
                                      self.w_up, self.w_down, self.dy)
 
 
-def run_layer(prob, world=None, cfg=None, reps=1, comm=None, keep=()):
+def run_layer(prob, world=None, cfg=None, reps=1, comm=None, keep=(), opts=None):
     """Runs fwd+bwd on `world` virtual ranks sharing cuda:0 (each with its own SM budget and
     stream). Returns per-rank outputs as numpy (bf16 as uint16); `keep` names internal buffers
     ("rep", "rep_dx": the [T*k][H] replica slots at the source) copied into the last rep's outputs."""
@@ -88,6 +88,9 @@ def run_layer(prob, world=None, cfg=None, reps=1, comm=None, keep=()):
     if comm is not None:
         for r in ranks:
             r.set_comm_options(*comm)
+    for name, val in (opts or {}).items():
+        for r in ranks:
+            r.set_option(name, val)
     streams = [torch.cuda.Stream() for _ in range(W)]
     ins = []
     for r in range(W):
@@ -178,6 +181,21 @@ def test_comm_workers_bitwise_invariant():
     ga, gb = gather(relay2[0]), gather(a2a2[0])
     for key in ("y", "dx", "dgate", "dw_up", "dw_down"):
         assert (ga[key] == gb[key]).all(), f"EP=2 relay+spare vs comm CTAs: {key}"
+
+
+def test_single_cta_engine_equals_cta_pair_engine():
+    """The single-CTA engine (cta_group::1, 128x256 tiles, 4 stages, the down-dgrad epilogue reading the
+    saved g/u with per-lane loads) and the default CTA-pair engine (cta_group::2, 256x256 tiles, the
+    down-dgrad epilogue's TMA input ring in its 5-stage mode) sum every output element over K in the same
+    ascending order: bit-identical results, at EP=1 and on two virtual ranks."""
+    for prob, world in ((Problem(1, 16, 4, 512, 768, 300, seed=9), None),
+                        (Problem(2, 8, 2, 256, 512, 200, seed=4), 2)):
+        pair, _, _ = run_layer(prob, world=world)
+        single, _, _ = run_layer(prob, world=world, opts={"engine_pair": 0})
+        gp, gs = gather(pair[0]), gather(single[0])
+        for key in ("y", "dx", "dgate", "dw_up", "dw_down"):
+            assert (gp[key] == gs[key]).all(), f"single vs pair engine: {key}"
+        check_vs_oracle(prob, gp)
 
 
 def test_token_map_bit_exact_vs_reference_fixture_ep2():

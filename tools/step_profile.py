@@ -15,6 +15,7 @@ ap.add_argument("--ncu", action="store_true")
 ap.add_argument("--out", default="gpurun_out")
 ap.add_argument("--cfg", default="")
 ap.add_argument("--sms", type=int, default=0, help="persistent-grid SM budget (0: all)")
+ap.add_argument("--opt", action="append", default=[], help="eplab_set_option name=value")
 args = ap.parse_args()
 H, F, E, k, T = bench.CONFIGS[args.config]
 sel, gw = po.Oracle().sample_routing(E, k, T, 1, 7)
@@ -28,6 +29,8 @@ if args.sms:
     L.set_sm_budget(args.sms)
 cfg = choose_config(H, F, E, k, T, 1, n_sm=args.sms or 148) if not args.cfg else M.TuneConfig(*[int(v) for v in args.cfg.split(",")])
 L.set_tune_config(cfg)
+for o in args.opt:
+    L.set_option(o.split("=")[0], int(o.split("=")[1]))
 y = torch.empty(T, H, device="cuda", dtype=torch.bfloat16)
 out = dict(dx=torch.empty(T, H, dtype=torch.bfloat16, device="cuda"), dw_up=torch.empty_like(w_up),
            dw_down=torch.empty_like(w_down), dgate=torch.empty(T, k, dtype=torch.float32, device="cuda"))

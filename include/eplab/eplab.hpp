@@ -12,6 +12,7 @@
 //   softfloat.hpp:10-28  FpFormat, round_to_bf16, fp_round, fp_add, fp_mul, bit_equal
 //   perf_model.hpp:38-62 effective_bandwidth ... predict_latency (reference-compatible)
 //   tuner.hpp:16-82      enumerate_space, search, TuneCache
+//   sim.hpp:16-85        Role, role_name, TaskQueueInfo, build_task_list (the task layout, not the simulator)
 // B200 additions: b200_hardware(), predict_layer() (fwd+bwd model of the MegaKernels built
 // here, incl. the relay-off AllToAll mode), search_layer().
 #pragma once
@@ -397,6 +398,25 @@ class TuneCache {
   std::map<std::tuple<std::string, std::string, long long>, TuneResult> entries_;
   long long invocations_ = 0;
 };
+
+// --------------------------------------------------------------- task list (sim.hpp:16-85, a9)
+// The MegaKernel's linearised task space of one rank: [comm | relay | comp] for Dispatch+GroupGEMM
+// (the reference's claim order; the device kernels claim the same order from one cursor). comm_slices
+// are contiguous ranges of the rank's send schedule, balanced by NVLink transmissions (the first
+// (token, dst rank) item of the priority order; a replica whose row a relay copy covers is free);
+// relay_ranges are even ranges of the up-GEMM tiles (rowgroups of b_m rows x ceil(2F / b_n) columns).
+// The discrete-event simulator of sim.hpp (run_*_sim) is not part of this build: the kernels are.
+enum class Role { Comm, Relay, Comp, Reduce };
+const char* role_name(Role r);
+struct TaskQueueInfo {
+  long long n_comm = 0, n_relay = 0, n_comp = 0, n_reduce = 0;
+  std::vector<std::pair<long long, long long>> comm_slices;    // send item ranges
+  std::vector<std::pair<long long, long long>> relay_ranges;   // tile ranges
+  std::vector<std::pair<long long, long long>> reduce_ranges;  // token ranges
+  long long total() const { return n_comm + n_relay + n_comp + n_reduce; }
+};
+TaskQueueInfo build_task_list(const MoEShape& shape, const TuneConfig& cfg, const RoutingInstance& routing,
+                              int rank);
 
 }  // namespace eplab
 #pragma GCC visibility pop

@@ -346,6 +346,12 @@ EPLAB_API int eplab_host_send_schedule(const int32_t* sel, int world, int n_exp,
                                        int topk, int rank, int64_t* item_token, int32_t* item_slot,
                                        int32_t* item_dst_rank, int32_t* item_dst_expert,
                                        int64_t* item_dst_offset);
+/* build_task_list (sim.hpp:84): one rank's dispatch-kernel task layout -- comm_slices [n_disp][2] (send
+ * schedule ranges balanced by NVLink transmissions), relay_ranges [n_relay][2] (up-GEMM tile ranges),
+ * n_comp (up-GEMM tiles). Routing sel [world][n_tok*topk] with the shape's n_exp, n_tok, topk. */
+EPLAB_API int eplab_host_build_task_list(const int32_t* sel, int world, const eplab_shape* s,
+                                         const eplab_tune_config* c, int rank, int64_t* comm_slices,
+                                         int64_t* relay_ranges, int64_t* n_comp);
 /* volume_expected (traffic.hpp:46); remote_only = SelfRankAccounting::RemoteOnly. */
 EPLAB_API int eplab_volume_expected(const eplab_shape* s, const eplab_hw* h, int remote_only,
                                     eplab_traffic* out);

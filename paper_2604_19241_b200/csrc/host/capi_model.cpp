@@ -170,6 +170,25 @@ int eplab_host_send_schedule(const int32_t* sel, int world, int n_exp, long long
   });
 }
 
+int eplab_host_build_task_list(const int32_t* sel, int world, const eplab_shape* s, const eplab_tune_config* c,
+                               int rank, int64_t* comm_slices, int64_t* relay_ranges, int64_t* n_comp) {
+  return guarded([&] {
+    if (world < 1 || s->n_exp % world) throw ValidationError("n_exp not divisible by world");
+    if (rank < 0 || rank >= world) throw ValidationError("rank out of range");
+    TaskQueueInfo tq = build_task_list(to_shape(s), TuneConfig{c->n_disp, c->n_relay, c->n_comb, c->n_red, c->w},
+                                       to_routing(sel, world, s->n_exp, s->n_tok, s->topk), rank);
+    for (size_t i = 0; i < tq.comm_slices.size(); ++i) {
+      comm_slices[2 * i] = tq.comm_slices[i].first;
+      comm_slices[2 * i + 1] = tq.comm_slices[i].second;
+    }
+    for (size_t i = 0; i < tq.relay_ranges.size(); ++i) {
+      relay_ranges[2 * i] = tq.relay_ranges[i].first;
+      relay_ranges[2 * i + 1] = tq.relay_ranges[i].second;
+    }
+    *n_comp = tq.n_comp;
+  });
+}
+
 int eplab_volume_expected(const eplab_shape* s, const eplab_hw* h, int remote_only,
                           eplab_traffic* out) {
   return guarded([&] {

@@ -125,6 +125,52 @@ def test_perf_model_and_tuner_vs_reference_build():
     assert lmin == rl and ev == rev == 277992
 
 
+def _task_list(sel, shape, cfg, rank):
+    L = lib()
+    sel = np.ascontiguousarray(sel, np.int32)
+    cs = np.zeros(2 * max(cfg.n_disp, 1), np.int64)
+    rr = np.zeros(2 * max(cfg.n_relay, 1), np.int64)
+    nc = C.c_longlong()
+    rc = L.eplab_host_build_task_list(_p(sel), sel.shape[0], C.byref(shape), C.byref(cfg), rank, _p(cs), _p(rr),
+                                      C.byref(nc))
+    assert rc == 0
+    return cs.reshape(-1, 2)[:cfg.n_disp], rr.reshape(-1, 2)[:cfg.n_relay], nc.value
+
+
+def test_build_task_list_contract():
+    """sim.cpp:226-250 semantics on a hand case: one rank -> nothing crosses a link, so the comm slices are the
+    even split of the schedule; relay ranges split the up-GEMM tiles evenly; slices tile their range."""
+    m = model()
+    T, k, E, F = 100, 2, 4, 512
+    sel = np.array([[(t + j) % E for t in range(T) for j in range(k)]], np.int32)
+    s, c = po.make_shape(1024, F, E, k, T), po.Cfg(3, 2, 1, 4, 8)
+    cs, rr, nc = _task_list(sel, s, c, 0)
+    rows = np.bincount(sel[0], minlength=E)                       # 50 rows per expert
+    assert nc == sum(-(-int(r) // 128) for r in rows) * (2 * F // 256)
+    assert cs.tolist() == [[0, 67], [67, 134], [134, 200]]        # 200 items, no transmissions
+    assert rr[0][0] == 0 and rr[-1][1] == nc and all(rr[i][1] == rr[i + 1][0] for i in range(len(rr) - 1))
+
+
+@needs_ref
+def test_build_task_list_vs_reference_build():
+    """eplab::build_task_list (the a9 task layout) equals the reference's on random routings: transmission-
+    balanced comm slices (world > 1), even relay tile ranges, the tile count."""
+    rng = np.random.default_rng(5)
+    for _ in range(40):
+        W = int(rng.choice([1, 2, 4, 8]))
+        E = W * int(rng.choice([1, 2, 4, 16]))
+        k = int(rng.integers(1, min(E, 8) + 1))
+        T = int(rng.integers(1, 600))
+        F = int(rng.choice([256, 768, 2048]))
+        sel = np.stack([np.concatenate([rng.permutation(E)[:k] for _ in range(T)]) for _ in range(W)]).astype(np.int32)
+        s = po.make_shape(int(rng.choice([1024, 2048])), F, E, k, T)
+        c = po.Cfg(int(rng.integers(0, 12)), int(rng.integers(0, 6)), 1, 8, 8)
+        for r in range(W):
+            a = _task_list(sel, s, c, r)
+            b = REF.build_task_list(sel, s, c, r)
+            assert (a[0] == b[0]).all() and (a[1] == b[1]).all() and a[2] == b[2], (W, E, k, T, c.tup(), r)
+
+
 def test_b200_layer_model_sanity():
     m = model()
     s = m.shape(4096, 14336, 8, 2, 16384)

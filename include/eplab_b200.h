@@ -148,7 +148,8 @@ EPLAB_API int eplab_set_comm_options(eplab_ctx* ctx, int spare_warps, int bulk_m
 /* Experiment knobs (A/B measurements; never read from the environment): "engine_pair" (1: CTA-pair
  * engine, 0: single-CTA), "spare" / "comm_bulk" (as eplab_set_comm_options), "rgp" / "tngp" /
  * "tngp_d" (raster groups of the NT / up-TN / down-TN pair tiles), "bwd_disp_scale" (comm CTAs of
- * the backward dispatch relative to the forward's), "dbg" (debug bits that SKIP work: results
+ * the backward dispatch relative to the forward's), "pdl" (1, default: the CTA-pair MegaKernels use
+ * programmatic dependent launch when the rank owns the whole device), "dbg" (debug bits that SKIP work: results
  * wrong, for measuring a role's share only). Unknown names return 2. */
 EPLAB_API int eplab_set_option(eplab_ctx* ctx, const char* name, int value);
 /* Persistent grid size (default: all SMs). Several ranks sharing one GPU (the single-device

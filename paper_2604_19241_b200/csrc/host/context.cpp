@@ -21,6 +21,9 @@
 
 using namespace eplab_dev;
 
+#ifndef EPLAB_PDL_DEFAULT
+#define EPLAB_PDL_DEFAULT 1
+#endif
 namespace {
 
 constexpr int kBM = 128;
@@ -84,7 +87,7 @@ struct eplab_ctx {
   int spare_warps = 3, comm_bulk = 0;
   // experiment knobs (eplab_set_option; never read from the environment): raster groups of the
   // NT / TN pair tiles, backward comm-CTA scale, debug bits (dbg != 0 gives WRONG results)
-  int rgp = 8, tngp = 4, tngp_d = 4, bwd_disp_scale = 2, dbg = 0;
+  int rgp = 8, tngp = 4, tngp_d = 4, bwd_disp_scale = 2, dbg = 0, pdl = EPLAB_PDL_DEFAULT;
   // EP > 1: relay on/off is a protocol choice every rank must share; fixed at init from the
   // shape and the device (identical on every rank, checked by the IPC layout signature)
   int relay_pref = -1, relay_pref_n = 0, dev_sms = 148;
@@ -199,6 +202,9 @@ MkArgs base_args(eplab_ctx* c) {
   a.rgp = c->rgp;
   a.tngp = c->tngp;
   a.tngp_d = c->tngp_d;  // profiles/r01_wgrad_raster.txt
+  // programmatic dependent launch only when this rank owns the whole device: ranks sharing a GPU
+  // (SM budgets) must not let one rank's early CTAs take SMs another rank's grid still needs
+  a.pdl = c->pdl && c->num_sms == c->dev_sms;
   // somebody must move the rows: the bulk mover and spare-less pools need >= 1 comm CTA
   if (a.n_disp == 0 && (a.comm_bulk || !(a.spare_warps & 1))) a.n_disp = 1;
   return a;
@@ -586,6 +592,8 @@ int eplab_set_option(eplab_ctx* c, const char* name, int value) {
     } else if (n == "rgp" || n == "tngp" || n == "tngp_d" || n == "bwd_disp_scale") {
       validate(value >= 1 && value <= 64, n + " must be in [1, 64]");
       (n == "rgp" ? c->rgp : n == "tngp" ? c->tngp : n == "tngp_d" ? c->tngp_d : c->bwd_disp_scale) = value;
+    } else if (n == "pdl") {
+      c->pdl = value != 0;
     } else if (n == "dbg") {
       c->dbg = value;  // experiments only: non-zero bits skip work and give wrong results
     } else {

@@ -1584,6 +1584,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int ph = (KIND >= 2) ? 1 : 0;
   const bool has_pre = (KIND == 0 || KIND == 2);
   const bool has_post = (KIND == 1 || KIND == 3);
+  // Programmatic dependent launch: let the next MegaKernel's CTAs take the SMs ours leave (it can only
+  // launch once every CTA of this grid has started), build this CTA's barriers and TMEM allocation
+  // while the previous kernel drains, and touch no global state before it has completed.
+  if (a.pdl) griddep_launch_dependents();
+  gemm_setup_pair(S, rank);
+  if (a.pdl) griddep_wait();
   load_epoch(a);
   if (blockIdx.x == 0) {
     const SymPtrs& me = a.peers.p[a.d.rank];
@@ -1592,8 +1598,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (has_post)
       for (int t = threadIdx.x; t < a.d.T_max; t += blockDim.x) *tok_counter(me, a.d, ph, (PAR(a) ^ 1), t) = 0;
   }
-  if (iteration_aborted(a)) return;  // both CTAs of the pair read the same words: no cluster sync yet
-  gemm_setup_pair(S, rank);
+  if (iteration_aborted(a)) {  // both CTAs of the pair read the same words and leave together
+    gemm_teardown_pair(S);
+    return;
+  }
   const int n_pre = has_pre ? a.n_disp + a.n_relay : 0;
   const int pairs = a.p.mpair_pre[a.d.epr];
   int n_tiles = 0;
@@ -1692,8 +1700,11 @@ static int launch_mk(const TmaSet& tm, const MkArgs& a, int grid, cudaStream_t s
   at[0].val.clusterDim.x = 2;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cudaLaunchAttribute at2[2] = {at[0], {}};
+  at2[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at2[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = a.pdl ? at2 : at;
+  cfg.numAttrs = a.pdl ? 2 : 1;
   cudaLaunchKernelEx(&cfg, fn, tm, a);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }

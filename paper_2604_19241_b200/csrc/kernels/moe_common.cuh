@@ -147,6 +147,8 @@ struct MkArgs {
   int comm_bulk;
   int rgp, tngp, tngp_d;  // CTA-pair raster groups: 256-row blocks per NT group, 256-row output
                           // blocks per TN group (up weight gradient / down weight gradient)
+  int pdl;  // launched with programmatic dependent launch (the whole device is this rank's: the CTAs
+            // start as the previous MegaKernel's exit, set up, then wait for its completion)
   // Unfused baseline: the same GroupGEMM tiles with every collective removed --
   // the rows were scattered into the receive layout before the launch (NCCL all-to-all), so no
   // scoreboard wait; the combine epilogues write each replica row to ret[ret_pos[slot]] (the

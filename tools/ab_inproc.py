@@ -17,6 +17,8 @@ ap.add_argument("--config", default="qwen3")
 ap.add_argument("--variants", required=True)
 ap.add_argument("--rounds", type=int, default=20)
 ap.add_argument("--shape", default="", help="H,F,E,k,T instead of a bench config")
+ap.add_argument("--whole", action="store_true",
+                help="events at step boundaries only (kernels back to back, e.g. for programmatic dependent launch)")
 args = ap.parse_args()
 H, F, E, k, T = [int(v) for v in args.shape.split(",")] if args.shape else bench.CONFIGS[args.config]
 if args.shape:
@@ -64,6 +66,13 @@ def apply(v):
 
 def step_timed():
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    if args.whole:
+        ev[0].record(st)
+        L.plan(ids, gws); L.dispatch_group_gemm(x, w_up); L.group_gemm_combine(w_down, y)
+        L._dispatch_bwd(dy, w_down, out); L._combine_bwd(w_up, out)
+        for e in ev[1:]:
+            e.record(st)
+        return ev
     ev[0].record(st)
     L.plan(ids, gws); L.dispatch_group_gemm(x, w_up); ev[1].record(st)
     L.group_gemm_combine(w_down, y); ev[2].record(st)

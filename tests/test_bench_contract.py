@@ -27,3 +27,29 @@ def test_reference_arm_json_contract():
     assert cb["value"] == line["value"] and cb["cores"] >= 1 and cb["kind"] in ("port", "reference") and cb["sample"]
     assert line["e2e"] == {"value": line["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_gpu_arm_json_contract():
+    """bench.py's GPU arm on the small config: every key of the driver contract, a roofline object for the
+    dominant kernel, e2e with the host copies counted, the launch count and the sampled clocks."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "small", "--steps", "3",
+                          "--warmup", "3", "--no-cpu-baseline", "--no-per-config"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches", "roofline", "clocks"):
+        assert key in line, key
+    assert line["steps"] == 3 and line["warmup"] == 3 and line["n_gpus"] == 1 and line["scaling"] == "weak"
+    assert line["value"] > 0 and abs(line["value"] - 4096 / (line["ms_per_step"] / 1e3)) < 1e-6 * line["value"]
+    assert line["gpu_launches"] == 7 * 3
+    r = line["roofline"]
+    assert r["bound"] == "tensor" and r["unit"] == "TFLOP/s" and 0 < r["frac"] < 1.2
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    e = line["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert "sm_mhz" in line["clocks"] and "reasons" in line["clocks"]

@@ -277,6 +277,23 @@ def make_inputs(cfg_name, world, rank):
                 w_down=torch.randn(epr, H, F, device="cuda", generator=g, dtype=torch.bfloat16) * F ** -0.5)
 
 
+def nvlink_kib(index):
+    """(tx, rx) KiB summed over this GPU's NVLinks from the driver's link data-payload counters
+    (`nvidia-smi nvlink -gt d`), or None where the links report nothing (a single-GPU box)."""
+    import re
+    try:
+        out = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", str(index)], capture_output=True,
+                             text=True, timeout=30).stdout
+    except Exception:
+        return None
+    tot = {"Tx": 0, "Rx": 0}
+    seen = False
+    for m in re.finditer(r"Data (Tx|Rx):\s*(\d+)", out):
+        tot[m.group(1)] += int(m.group(2))
+        seen = True
+    return (tot["Tx"], tot["Rx"]) if seen else None
+
+
 def timed_steps(step, K, st, barrier):
     """K steps bracketed by barrier + synchronize, one event per step boundary on the launching
     stream: (mean ms over the bracket, median ms of the per-step intervals)."""
@@ -431,8 +448,14 @@ def run_ours(args):
     clocks.start()
     time.sleep(0.5)
     clocks.mark_start()
+    nvl0 = nvlink_kib(local) if world > 1 else None
     ms, ms_med = timed_steps(step, args.steps, st, barrier)
+    nvl1 = nvlink_kib(local) if world > 1 else None
     clocks.mark_end()
+    # NVLink payload bytes this GPU sent / received per step during the timed steps (link counters; the
+    # barriers around the region add a few KiB)
+    nvl = [(nvl1[0] - nvl0[0]) * 1024.0 / args.steps, (nvl1[1] - nvl0[1]) * 1024.0 / args.steps] \
+        if nvl0 and nvl1 else [-1.0, -1.0]
     clk = clocks.stop()
     layer.check()
     # ---- the same steps replayed from one captured CUDA graph (plan + 4 MegaKernels + memsets):
@@ -524,7 +547,8 @@ def run_ours(args):
     # ---- max over ranks
     names = list(kms)
     v = max_over_ranks([ms, ms_med, ms_e2e, ms_e2e_blocking, ms_graph or 0.0, unf_ms or 0.0, unf_med or 0.0]
-                       + [kms[n] for n in names])
+                       + [kms[n] for n in names] + nvl)
+    nvl = v[7 + len(names):]
     ms, ms_med, ms_e2e, ms_e2e_blocking = v[0], v[1], v[2], v[3]
     ms_graph, unf_ms, unf_med = v[4] or None, v[5] or None, v[6] or None
     kms = {n: v[7 + j] for j, n in enumerate(names)}
@@ -578,6 +602,16 @@ def run_ours(args):
             "clocks": clk,
             "cpu_baseline": cpu,
         }
+        if world > 1:
+            nvl_alg = algorithmic(args.config, world)[1] * T  # per GPU per direction per step
+            line["nvlink"] = (
+                {"tx_bytes_per_step_max": nvl[0], "rx_bytes_per_step_max": nvl[1],
+                 "tx_GBps_max": nvl[0] / (ms / 1e3) / 1e9, "rx_GBps_max": nvl[1] / (ms / 1e3) / 1e9,
+                 "algorithmic_bytes_per_step": nvl_alg,
+                 "frac_of_900GBps_over_step": max(nvl) / (ms / 1e3) / 900e9,
+                 "source": "nvidia-smi nvlink -gt d (link data payload) before/after the timed steps, max over ranks; "
+                           "GB/s averaged over the whole step (the comm roles run inside the MegaKernels)"}
+                if min(nvl) >= 0 else {"unavailable": "the NVLink counters report no data on this box"})
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

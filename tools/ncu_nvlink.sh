@@ -5,6 +5,10 @@
 # BYTES are exact, the GB/s below divide them by the duration each kernel has inside the real
 # (unprofiled) run, taken from bench.py's kernel_ms of the same command without ncu.
 #   usage: bash tools/ncu_nvlink.sh [N=8] [configs...]      (an N-GPU node; not the 1-GPU gpurun box)
+# Caveat: if the profiler serialises the ranks' kernels, a MegaKernel whose tiles wait for a peer's rows
+# cannot finish while that peer's kernel is held back: the scoreboard watchdog then ends the step with
+# error 3 instead of hanging. bench.py's own `nvlink` object (link payload counters around the timed
+# steps, no profiler) is the primary NVLink evidence; this capture adds per-kernel bytes when it completes.
 N=${1:-8}; shift
 mkdir -p gpurun_out
 M=gpu__time_duration.sum,nvltx__bytes.sum,nvlrx__bytes.sum,nvltx__bytes_data_user.sum,nvlrx__bytes_data_user.sum,dram__bytes_read.sum,dram__bytes_write.sum

@@ -532,3 +532,31 @@ class RouterFunction(torch.autograd.Function):
         if d_gw is None:
             return None, None, None
         return router_topk_bwd(logits, ids, gw, d_gw, ctx.renorm), None, None
+
+
+class MoELayer(torch.nn.Module):
+    """A trainable MoE FFN block on the MegaKernels: router (fp32 logits = x W_gate, softmax top-k on the
+    device, RouterFunction) -> EpMoEFunction (dispatch + up GroupGEMM + SwiGLU, down GroupGEMM + combine,
+    and their backward). Parameters: gate [H][E] fp32, this rank's experts w_up [E_loc][2F][H] and
+    w_down [E_loc][H][F] bf16. x [n_tok][H] bf16 -> y [n_tok][H] bf16; gradients reach x (through both
+    the experts and the router), the gate and the expert weights. Multi-rank: one module per rank,
+    connected with `self.experts.connect_distributed()` before the first forward."""
+
+    def __init__(self, hidden, ffn, n_experts, topk, max_tokens, rank=0, world=1, renorm=True, device=None,
+                 seed=0):
+        super().__init__()
+        self.experts = EpMoE(hidden, ffn, n_experts, topk, max_tokens, rank=rank, world=world, device=device)
+        dev = self.experts.device
+        g = torch.Generator(device=dev).manual_seed(seed + rank)
+        epr = n_experts // world
+        self.gate = torch.nn.Parameter(torch.randn(hidden, n_experts, device=dev, generator=g) * hidden ** -0.5)
+        self.w_up = torch.nn.Parameter(
+            (torch.randn(epr, 2 * ffn, hidden, device=dev, generator=g) * hidden ** -0.5).bfloat16())
+        self.w_down = torch.nn.Parameter(
+            (torch.randn(epr, hidden, ffn, device=dev, generator=g) * ffn ** -0.5).bfloat16())
+        self.topk, self.renorm = topk, renorm
+
+    def forward(self, x):
+        logits = x.float() @ self.gate
+        ids, gw = RouterFunction.apply(logits, self.topk, self.renorm)
+        return EpMoEFunction.apply(self.experts, x, ids, gw, self.w_up, self.w_down)

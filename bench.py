@@ -115,6 +115,12 @@ def hbm_bytes_per_step(cfg_name, world):
     """Algorithmic HBM bytes of one fwd+bwd step on one GPU (balanced routing): every tensor of
     the layer read or written once per use: the dispatch copies, both GEMMs' operands
     and outputs, the saved activations, replica slots, the reductions, the weight gradients."""
+    return float(sum(hbm_bytes_per_kernel(cfg_name, world).values()))
+
+
+def hbm_bytes_per_kernel(cfg_name, world):
+    """hbm_bytes_per_step split over the four MegaKernels (the roofline object compares the dominant
+    kernel's ncu DRAM traffic with its share)."""
     H, F, E, k, T = CONFIGS[cfg_name]
     R = T * k                      # rows received per GPU (balanced)
     El = E // world
@@ -125,7 +131,8 @@ def hbm_bytes_per_step(cfg_name, world):
     bwd_d = T * row + R * row + R * row + w_down + R * 2 * F * 2 + R * 2 * F * 2 + R * F * 2 \
         + R * row + R * F * 2 + w_down
     bwd_c = R * 4 * F + w_up + R * row + R * 4 * F + R * row + w_up + T * k * row + T * row
-    return float(fwd_d + fwd_c + bwd_d + bwd_c)
+    return {"fwd_dispatch_gemm": float(fwd_d), "fwd_gemm_combine": float(fwd_c), "bwd_dispatch_gemm": float(bwd_d),
+            "bwd_gemm_combine": float(bwd_c)}
 
 
 def algorithmic(cfg_name, world):
@@ -582,6 +589,7 @@ def run_ours(args):
             "gpu_launches": 7 * args.steps,  # per step: 3 planning kernels + the 4 MegaKernels
             "roofline": {"bound": "tensor", "achieved": ach, "peak": peak_sust, "unit": "TFLOP/s",
                          "frac": ach / peak_sust, "traffic": traffic, "kernel": dom,
+                         "algorithmic_bytes": hbm_bytes_per_kernel(args.config, world)[dom],
                          "peak_source": f"{peak_src} bf16 sustained (kernel timed inside the step)",
                          "frac_of_burst": ach / peak_burst},
             "roofline_step": roofline_terms(args.config, world, ms),

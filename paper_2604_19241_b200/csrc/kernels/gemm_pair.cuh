@@ -66,6 +66,7 @@ __device__ __forceinline__ void gemm_setup_pair(GemmSmem* S, uint32_t rank) {
     S->bcast = TASK_STOP;
     fence_mbar_init();
   }
+  __syncthreads();  // thread 0's writes (S->bcast shares a 16-byte word with S->tmem_base) before the allocation
   if (warp == 2) tmem_alloc_pair(&S->tmem_base, TMEM_COLS);
   tc_fence_before();
   cluster_sync_all();

@@ -111,17 +111,14 @@ def _full_size_checks(layer, H, F, E, k, T, sel, gw, x, dy, w_up, w_down, ids, g
     assert_ulp(a["dgate"][toks].cpu().numpy().reshape(-1), ref["dgate"].reshape(-1), "dgate", "dgate")
 
 
-@pytest.mark.parametrize("relay", [0, 4])
-def test_world_invariance_full_size_qwen3_ep8(relay):
-    """Qwen3 shape (128 experts, top-8, H 2048, F 768) with 16K tokens per rank on 8 virtual
-    ranks (one process, 18 SMs each, peer rows through the same symmetric buffers the NVLink path
-    uses) equals EP=1 on the same 131K tokens bit for bit -- y, dx, dgate, dW -- with the
-    AllToAll-style (relay off) and AllGather-style (relay on) dispatch."""
+def _world_invariance(cfg, W, T, relay, n_disp=4, seed=3):
+    """cfg's layer with T tokens per rank on W virtual ranks (one process, 148/W SMs each, peer rows
+    through the same symmetric buffers the NVLink path uses) == EP=1 on the same W*T tokens, bit for bit:
+    y, dx, dgate, dW_up, dW_down."""
     from paper_2604_19241_b200 import moe as M
     from paper_2604_19241_b200.model import sample_routing
-    H, F, E, k, T = SHAPES["qwen3"]
-    W = 8
-    sel, gw = sample_routing(E, k, T, W, 3)  # [W][T*k]: rank r's tokens are global tokens r*T..
+    H, F, E, k, _ = SHAPES[cfg]
+    sel, gw = sample_routing(E, k, T, W, seed)  # [W][T*k]: rank r's tokens are global tokens r*T..
     g = torch.Generator(device="cuda").manual_seed(5)
     x = torch.randn(W * T, H, device="cuda", generator=g).bfloat16()
     dy = (torch.randn(W * T, H, device="cuda", generator=g) * 0.5).bfloat16()
@@ -136,14 +133,14 @@ def test_world_invariance_full_size_qwen3_ep8(relay):
     one.check()
     torch.cuda.synchronize()
     one.close()
-    # EP=8: 16 experts and T tokens per virtual rank (receive capacity for balanced routing + slack)
+    # EP=W: E/W experts and T tokens per virtual rank (receive capacity for balanced routing + slack)
     epr = E // W
-    ranks = [M.EpMoE(H, F, E, k, T, rank=r, world=W, max_recv_rows=T * k * 5 // 4, timeout_s=60.0)
+    ranks = [M.EpMoE(H, F, E, k, T, rank=r, world=W, max_recv_rows=T * k * 5 // 4 + 128 * epr, timeout_s=60.0)
              for r in range(W)]
     M.EpMoE.connect_local(ranks)
     for r in ranks:
         r.set_sm_budget(148 // W)
-        r.set_tune_config((4, relay, 1, 148 // W, 8))
+        r.set_tune_config((n_disp, relay, 1, 148 // W, 8))
     streams = [torch.cuda.Stream() for _ in range(W)]
     torch.cuda.synchronize()
     ys, gs = [None] * W, [None] * W
@@ -171,6 +168,23 @@ def test_world_invariance_full_size_qwen3_ep8(relay):
     assert torch.equal(torch.cat([gg["dw_down"] for gg in gs]), g1["dw_down"]), "dw_down"
     for r in ranks:
         r.close()
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("relay", [0, 4])
+def test_world_invariance_full_size_qwen3_ep8(relay):
+    """Qwen3 shape (128 experts, top-8, H 2048, F 768) with 16K tokens per rank on 8 virtual ranks equals
+    EP=1 on the same 131K tokens bit for bit, with the AllToAll-style (relay off) and AllGather-style
+    (relay on) dispatch."""
+    _world_invariance("qwen3", 8, SHAPES["qwen3"][4], relay)
+
+
+@pytest.mark.parametrize("W,T,relay", [(2, 16384, 0), (8, 4096, 0), (8, 4096, 2)])
+def test_world_invariance_mixtral(W, T, relay):
+    """The bench's Mixtral shape (8 experts top-2, H 4096, F 14336): 16K tokens per rank at EP=2, and 4K
+    tokens per rank at EP=8 (one expert per rank, relay off and on) equal EP=1 on the same tokens bit for
+    bit -- the GPU-count invariance of the headline configuration."""
+    _world_invariance("mixtral", W, T, relay)
 
 
 def test_small_config_ep2_full_size():

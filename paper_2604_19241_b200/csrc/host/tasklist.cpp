@@ -57,8 +57,9 @@ Ranges split_by_transmissions(const std::vector<char>& sends, long long parts) {
 
 TaskQueueInfo build_task_list(const MoEShape& shape, const TuneConfig& cfg, const RoutingInstance& routing,
                               int rank) {
+  if (rank < 0 || rank >= routing.world) throw ValidationError("rank out of range");
   const std::vector<GlobalTokenMap> maps = build_global_token_map(routing);
-  const GlobalTokenMap& map = maps.at((size_t)rank);
+  const GlobalTokenMap& map = maps[(size_t)rank];
   // up-GEMM tiles of this rank: rowgroups of b_m rows per local expert segment x column tiles of 2F
   const long long col_tiles = (2LL * shape.h_inter + shape.b_n - 1) / shape.b_n;
   long long rowgroups = 0, received = 0;

@@ -547,9 +547,11 @@ class MoELayer(torch.nn.Module):
         super().__init__()
         self.experts = EpMoE(hidden, ffn, n_experts, topk, max_tokens, rank=rank, world=world, device=device)
         dev = self.experts.device
-        g = torch.Generator(device=dev).manual_seed(seed + rank)
         epr = n_experts // world
+        # the router is replicated (the same gate on every rank); the experts are this rank's shard
+        g = torch.Generator(device=dev).manual_seed(seed)
         self.gate = torch.nn.Parameter(torch.randn(hidden, n_experts, device=dev, generator=g) * hidden ** -0.5)
+        g = torch.Generator(device=dev).manual_seed(seed + 1 + rank)
         self.w_up = torch.nn.Parameter(
             (torch.randn(epr, 2 * ffn, hidden, device=dev, generator=g) * hidden ** -0.5).bfloat16())
         self.w_down = torch.nn.Parameter(
